@@ -85,10 +85,11 @@ enum hda_part_kind { HDA_ROW = 0, HDA_COL = 1, HDA_BLOCK = 2 };
  *                    (Listing 2; A,B bf16, C f32 or bf16, fp32 accumulate
  *                    on tensor cores; scalars = {alpha, beta}; uses A (0,*), B (*,0),
  *                    C (0,0) iff beta != 0)
- *  HDA_K_STAMP       [X]            every cell c of the composed DEF set of device p
+ *  HDA_K_STAMP       [X, Y...]      every cell c of the composed DEF set of device p
  *                    gets the low bytes of splitmix64(seed*0x9E3779B97F4A7C15 + c)
  *                    (c = linear index; scalars[0] = seed); a test kernel that
- *                    writes arbitrary def shapes with distinctive raw bits.
+ *                    writes arbitrary def shapes with distinctive raw bits.  Extra
+ *                    parameters Y may declare uses (their data moves) but no defs.
  * Built-in kernels other than NONE/STAMP require def offsets == {(0,..,0)} and
  * declared uses covering their true footprint (EINVAL), and work ⊕ footprint
  * inside the array (ERANGE).  An array used at a non-zero offset and defined in

@@ -611,9 +611,9 @@ static int nparams(int kernel) {
     case ORC_K_COPY:
     case ORC_K_STENCIL9:
     case ORC_K_STENCIL7_3D: return 2;
-    case ORC_K_SCALE:
-    case ORC_K_STAMP: return 1;
+    case ORC_K_SCALE: return 1;
     case ORC_K_GEMM: return 3;
+    case ORC_K_STAMP: /* [X, used...] */
     case ORC_K_NONE: return -1; /* any */
   }
   return -2;
@@ -659,7 +659,11 @@ int orc_apply(orc_t* w, int kernel, int part, int n_acc, const int32_t* arrays,
     for (int e = 1; e < n_acc; e++)
       if (n_def[e] != 0) return fail(w, ORC_EINVAL, "only param 0 may be defined");
   }
-  if (kernel == ORC_K_STAMP && n_scalars < 1) return fail(w, ORC_EINVAL, "STAMP needs seed");
+  if (kernel == ORC_K_STAMP) {
+    if (n_acc < 1 || n_scalars < 1) return fail(w, ORC_EINVAL, "STAMP needs [X, ...] and a seed");
+    for (int e = 1; e < n_acc; e++)
+      if (n_def[e] != 0) return fail(w, ORC_EINVAL, "STAMP defines only param 0");
+  }
   if (kernel == ORC_K_SCALE && n_scalars < 1) return fail(w, ORC_EINVAL, "SCALE needs alpha");
   if (kernel == ORC_K_GEMM && n_scalars < 2) return fail(w, ORC_EINVAL, "GEMM needs alpha, beta");
   int64_t fp[8][3];

@@ -1,0 +1,1235 @@
+// hda.cpp — runtime and C-ABI of the B200-native HDArray hot path (see include/hdarray.h).
+//
+// Per hda_apply (Table 2 ApplyKernel):
+//   1. tracker: compose LUSE/LDEF + plan (Eq. 1-2), or a plan-cache hit
+//   2. exchange: every planned rectangle moves from its last writer to its reader
+//      FUSED : one copy kernel on the reader's GPU loads the writer's replica through
+//              NVLink peer memory and stores into its own replica (pack + transfer +
+//              unpack in one pass, no staging)
+//      STAGED: pack kernel on the writer -> copy engine -> unpack kernel on the reader
+//   3. the built-in kernel on every local device's work box
+//   4. tracker commit (Eq. 3-4 corrected), on the host while the GPUs run
+//
+// Sync protocol (no host barriers; works across processes through CUDA IPC):
+// every device d owns 192 monotone 64-bit words in its own HBM:
+//   PROD[p]  = last call epoch whose kernel/write on device p has completed (written by p)
+//   PACK[p]  = last epoch for which p's staged payload for d is packed     (written by p)
+//   ACK[r]   = last epoch at which device r finished reading from d       (written by r)
+// A reader waits PROD[p] >= epoch of p's last definition before pulling (RAW); a
+// writer waits ACK[r] >= epoch of r's last pull before overwriting (WAR).  Waits are
+// 1-block spin kernels with a timeout (sticky HDA_ETIMEOUT, never a hang); signals
+// are release stores at system scope.  Devices that share a CUDA stream (virtual
+// devices on one GPU) are ordered by the stream and skip both.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "hdarray.h"
+#include "kernels.cuh"
+#include "tracker.hpp"
+
+using namespace hda;
+
+namespace {
+
+constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_WORDS = 192;
+constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
+
+struct Gpu {
+  int ordinal = 0;
+  cudaStream_t stream = nullptr;
+};
+
+struct Dev {
+  bool local = false;
+  int gpu = -1;                        // index into ctx->gpus (local devices)
+  unsigned long long* sync = nullptr;  // this device's sync words (local or IPC-mapped)
+  bool sync_alloc = false, sync_ipc = false;
+};
+
+struct ArrRT {
+  std::vector<char*> ptr;  // per device: local replica, IPC-mapped peer replica, or null
+  std::vector<char> alloc, ipc;
+  bool imported = false;
+  size_t bytes = 0;
+};
+
+struct TimedEv {
+  int kind;  // kernel id, or -100 for exchange
+  cudaEvent_t a, b;
+};
+
+struct PullJob {
+  int dst;
+  std::vector<int> srcs;
+  std::vector<RunBatch> batches;
+  std::vector<std::pair<int, int>> pend;  // (array, src) pairs read by this pull
+};
+struct PackJob {
+  int src;
+  std::vector<int> dsts;
+  std::vector<RunBatch> batches;
+  size_t bytes = 0;
+};
+struct Seg {
+  int src;
+  size_t src_off, dst_off, bytes;
+};
+struct RecvJob {
+  int dst;
+  std::vector<int> srcs;
+  std::vector<Seg> segs;
+  std::vector<RunBatch> unpack;
+  size_t bytes = 0;
+};
+struct ExecPlan {
+  bool staged = false;
+  std::vector<PullJob> pulls;
+  std::vector<PackJob> packs;
+  std::vector<RecvJob> recvs;
+};
+
+}  // namespace
+
+struct hda_ctx {
+  int P = 0;
+  bool spmd = false, plan_only = false, sync_imported = true;
+  int rank = -1;
+  std::vector<Gpu> gpus;
+  std::vector<Dev> dev;
+  std::unique_ptr<Tracker> tr;
+  std::vector<ArrRT> arr;
+  unsigned long long epoch = 0;
+  std::vector<unsigned long long> last_prod;
+  std::vector<std::vector<std::vector<unsigned long long>>> pend;  // [array][src][dst]
+  std::vector<std::vector<std::pair<int, unsigned long long>>> stage_pend;  // [src]
+  std::vector<char*> send_stage, recv_stage;
+  std::vector<size_t> send_cap, recv_cap;
+  std::unordered_map<uint64_t, ExecPlan> exec;
+  int transport = HDA_XPORT_FUSED;
+  bool cache_on = true, ktiming = false;
+  std::vector<TimedEv> tev;
+  std::vector<cudaEvent_t> ev_pool;
+  double ktime_ms[KN_COUNT] = {};
+  int64_t kcount[KN_COUNT] = {};
+  double xtime_ms = 0;
+  int64_t xcount = 0;
+  int* err_host = nullptr;
+  int sticky = 0;
+  std::string err;
+  hda_stats_t stats{};
+  std::vector<hda_msg_t> last_plan;
+  long long timeout_ns = 60LL * 1000 * 1000 * 1000;
+};
+
+// ====================================================================== helpers
+
+static int fail(hda_ctx_t* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return code;
+}
+
+static int cuda_fail(hda_ctx_t* c, cudaError_t e, const char* what) {
+  c->sticky = HDA_ECUDA;
+  c->err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return HDA_ECUDA;
+}
+
+#define CK(x)                                          \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #x); \
+  } while (0)
+
+#define GUARD()                                              \
+  do {                                                       \
+    if (!ctx) return HDA_EINVAL;                             \
+    if (ctx->sticky) return fail(ctx, ctx->sticky, ctx->err); \
+  } while (0)
+
+struct DevGuard {
+  int prev = -1;
+  bool on;
+  explicit DevGuard(bool enable) : on(enable) {
+    if (on) cudaGetDevice(&prev);
+  }
+  ~DevGuard() {
+    if (on && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+static void front_shape(int ndim, const int64_t* s, int64_t* out) {
+  int off = 3 - ndim;
+  for (int k = 0; k < 3; k++) out[k] = k < off ? 1 : s[k - off];
+}
+static Box front_box(int ndim, const Box& b) {
+  Box r = unit_box();
+  int off = 3 - ndim;
+  for (int k = 0; k < ndim; k++) {
+    r.lb[k + off] = b.lb[k];
+    r.ub[k + off] = b.ub[k];
+  }
+  return r;
+}
+
+static bool same_stream(const hda_ctx_t* ctx, int p, int q) {
+  return ctx->dev[p].local && ctx->dev[q].local && ctx->dev[p].gpu == ctx->dev[q].gpu;
+}
+
+static cudaStream_t stream_of(const hda_ctx_t* ctx, int d) { return ctx->gpus[ctx->dev[d].gpu].stream; }
+static int ordinal_of(const hda_ctx_t* ctx, int d) { return ctx->gpus[ctx->dev[d].gpu].ordinal; }
+
+// strided descriptor of box `fb` (front-padded) in an array of front-padded shape S
+static RunDesc rect_desc(const int64_t* S, const Box& fb, size_t es) {
+  RunDesc d;
+  std::memset(&d, 0, sizeof d);
+  const int64_t e0 = fb.ub[0] - fb.lb[0], e1 = fb.ub[1] - fb.lb[1], e2 = fb.ub[2] - fb.lb[2];
+  const int64_t off = ((fb.lb[0] * S[1] + fb.lb[1]) * S[2] + fb.lb[2]) * (int64_t)es;
+  d.src_off = d.dst_off = off;
+  d.es = (int32_t)es;
+  if (e2 == S[2] && e1 == S[1]) {
+    d.run_bytes = e0 * e1 * e2 * (int64_t)es;
+    d.n0 = 1;
+    d.n1 = 1;
+  } else if (e2 == S[2]) {
+    d.run_bytes = e1 * e2 * (int64_t)es;
+    d.n0 = (int32_t)e0;
+    d.n1 = 1;
+    d.src_p0 = d.dst_p0 = S[1] * S[2] * (int64_t)es;
+  } else {
+    d.run_bytes = e2 * (int64_t)es;
+    d.n0 = (int32_t)e0;
+    d.n1 = (int32_t)e1;
+    d.src_p0 = d.dst_p0 = S[1] * S[2] * (int64_t)es;
+    d.src_p1 = d.dst_p1 = S[2] * (int64_t)es;
+  }
+  return d;
+}
+
+static void batch_descs(std::vector<RunDesc>& descs, std::vector<RunBatch>& out) {
+  RunBatch b;
+  std::memset(&b, 0, sizeof b);
+  for (RunDesc d : descs) {
+    if (b.n == kMaxRunDescs) {
+      out.push_back(b);
+      std::memset(&b, 0, sizeof b);
+    }
+    int64_t u = run_desc_units(d);
+    if (u == 0) continue;
+    d.unit_begin = b.total_units;
+    b.total_units += u;
+    b.d[b.n++] = d;
+  }
+  if (b.n) out.push_back(b);
+}
+
+static void count_launch(hda_ctx_t* ctx, int n = 1) { ctx->stats.kernel_launches += n; }
+
+static cudaEvent_t get_event(hda_ctx_t* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+static int launch_waits(hda_ctx_t* ctx, int d, const WaitList& w) {
+  if (w.n == 0) return HDA_OK;
+  CK(launch_wait(w, ctx->err_host, ctx->timeout_ns, stream_of(ctx, d)));
+  count_launch(ctx);
+  return HDA_OK;
+}
+static int launch_signals(hda_ctx_t* ctx, int d, const SignalList& s) {
+  if (s.n == 0) return HDA_OK;
+  CK(launch_signal(s, stream_of(ctx, d)));
+  count_launch(ctx);
+  return HDA_OK;
+}
+static void wl_add(WaitList& w, unsigned long long* p, unsigned long long v) {
+  if (v == 0) return;
+  for (int i = 0; i < w.n; i++)
+    if (w.ptr[i] == p) {
+      if (w.val[i] < v) w.val[i] = v;
+      return;
+    }
+  w.ptr[w.n] = p;
+  w.val[w.n] = v;
+  w.n++;
+}
+
+static int check_err_flag(hda_ctx_t* ctx) {
+  if (ctx->err_host && *(volatile int*)ctx->err_host) {
+    ctx->sticky = HDA_ETIMEOUT;
+    ctx->err = "a cross-device wait timed out (a peer did not signal)";
+    return HDA_ETIMEOUT;
+  }
+  return HDA_OK;
+}
+
+static int sync_all(hda_ctx_t* ctx) {
+  for (auto& g : ctx->gpus) {
+    CK(cudaSetDevice(g.ordinal));
+    CK(cudaStreamSynchronize(g.stream));
+  }
+  return check_err_flag(ctx);
+}
+
+// ====================================================================== exec plans
+
+static int ensure_stage(hda_ctx_t* ctx, std::vector<char*>& v, std::vector<size_t>& cap, int d, size_t need) {
+  if (cap[d] >= need) return HDA_OK;
+  CK(cudaSetDevice(ordinal_of(ctx, d)));
+  CK(cudaStreamSynchronize(stream_of(ctx, d)));
+  if (v[d]) CK(cudaFree(v[d]));
+  size_t n = std::max(need, (size_t)1 << 20);
+  CK(cudaMalloc((void**)&v[d], n));
+  cap[d] = n;
+  return HDA_OK;
+}
+
+static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
+  const int P = ctx->P;
+  ep.staged = ctx->transport == HDA_XPORT_STAGED;
+  if (t->msgs.empty()) return HDA_OK;
+  if (!ep.staged) {
+    for (int q = 0; q < P; q++) {
+      if (!ctx->dev[q].local) continue;
+      PullJob job;
+      job.dst = q;
+      std::vector<RunDesc> descs;
+      for (const Msg& m : t->msgs) {
+        if (m.dst != q) continue;
+        const TArray& a = ctx->tr->array(m.array);
+        int64_t S[3];
+        front_shape(a.ndim, a.shape, S);
+        RunDesc d = rect_desc(S, front_box(a.ndim, m.box), a.es);
+        d.src = ctx->arr[m.array].ptr[m.src];
+        d.dst = ctx->arr[m.array].ptr[q];
+        if (!d.src || !d.dst) return fail(ctx, HDA_ESTATE, "replica not mapped (SPMD handles missing?)");
+        descs.push_back(d);
+        if (std::find(job.srcs.begin(), job.srcs.end(), m.src) == job.srcs.end()) job.srcs.push_back(m.src);
+        std::pair<int, int> pr(m.array, m.src);
+        if (std::find(job.pend.begin(), job.pend.end(), pr) == job.pend.end()) job.pend.push_back(pr);
+      }
+      if (descs.empty()) continue;
+      batch_descs(descs, job.batches);
+      ep.pulls.push_back(std::move(job));
+    }
+    return HDA_OK;
+  }
+  // STAGED: p's send staging holds its outgoing messages ordered by (dst, array, lb),
+  // 256-byte aligned per message, so each (p, q) pair is one contiguous segment.
+  std::vector<const Msg*> order;
+  for (const Msg& m : t->msgs) order.push_back(&m);
+  std::stable_sort(order.begin(), order.end(), [](const Msg* a, const Msg* b) {
+    if (a->src != b->src) return a->src < b->src;
+    return a->dst < b->dst;
+  });
+  std::vector<size_t> src_off(order.size());
+  std::vector<size_t> used(P, 0);
+  for (size_t i = 0; i < order.size(); i++) {
+    const Msg& m = *order[i];
+    const TArray& a = ctx->tr->array(m.array);
+    src_off[i] = used[m.src];
+    used[m.src] += ((size_t)box_volume(m.box) * a.es + 255) & ~(size_t)255;
+  }
+  for (int p = 0; p < P; p++) {
+    if (!ctx->dev[p].local || used[p] == 0) continue;
+    int rc = ensure_stage(ctx, ctx->send_stage, ctx->send_cap, p, used[p]);
+    if (rc) return rc;
+  }
+  // packs
+  for (int p = 0; p < P; p++) {
+    if (!ctx->dev[p].local || used[p] == 0) continue;
+    PackJob job;
+    job.src = p;
+    job.bytes = used[p];
+    std::vector<RunDesc> descs;
+    for (size_t i = 0; i < order.size(); i++) {
+      const Msg& m = *order[i];
+      if (m.src != p) continue;
+      const TArray& a = ctx->tr->array(m.array);
+      int64_t S[3];
+      front_shape(a.ndim, a.shape, S);
+      RunDesc d = rect_desc(S, front_box(a.ndim, m.box), a.es);
+      d.src = ctx->arr[m.array].ptr[p];
+      d.dst = ctx->send_stage[p];
+      d.dst_off = (int64_t)src_off[i];
+      d.dst_p1 = d.run_bytes;
+      d.dst_p0 = d.run_bytes * d.n1;
+      descs.push_back(d);
+      if (std::find(job.dsts.begin(), job.dsts.end(), m.dst) == job.dsts.end()) job.dsts.push_back(m.dst);
+    }
+    batch_descs(descs, job.batches);
+    ep.packs.push_back(std::move(job));
+  }
+  // receives
+  for (int q = 0; q < P; q++) {
+    if (!ctx->dev[q].local) continue;
+    RecvJob job;
+    job.dst = q;
+    size_t off = 0;
+    std::vector<RunDesc> descs;
+    for (size_t i = 0; i < order.size(); i++) {
+      const Msg& m = *order[i];
+      if (m.dst != q) continue;
+      const TArray& a = ctx->tr->array(m.array);
+      size_t bytes = (size_t)box_volume(m.box) * a.es;
+      size_t padded = (bytes + 255) & ~(size_t)255;
+      if (!job.segs.empty() && job.segs.back().src == m.src &&
+          job.segs.back().src_off + job.segs.back().bytes == src_off[i]) {
+        job.segs.back().bytes += padded;
+      } else {
+        job.segs.push_back(Seg{m.src, src_off[i], off, padded});
+      }
+      int64_t S[3];
+      front_shape(a.ndim, a.shape, S);
+      RunDesc d = rect_desc(S, front_box(a.ndim, m.box), a.es);
+      d.dst = ctx->arr[m.array].ptr[q];
+      d.src_off = (int64_t)off;
+      d.src_p1 = d.run_bytes;
+      d.src_p0 = d.run_bytes * d.n1;
+      descs.push_back(d);
+      off += padded;
+      if (std::find(job.srcs.begin(), job.srcs.end(), m.src) == job.srcs.end()) job.srcs.push_back(m.src);
+    }
+    if (descs.empty()) continue;
+    job.bytes = off;
+    int rc = ensure_stage(ctx, ctx->recv_stage, ctx->recv_cap, q, off);
+    if (rc) return rc;
+    for (RunDesc& d : descs) d.src = ctx->recv_stage[q];
+    batch_descs(descs, job.unpack);
+    ep.recvs.push_back(std::move(job));
+  }
+  return HDA_OK;
+}
+
+// ====================================================================== phases
+
+static int timed_begin(hda_ctx_t* ctx, int d, cudaEvent_t* a) {
+  *a = nullptr;
+  if (!ctx->ktiming) return HDA_OK;
+  *a = get_event(ctx);
+  CK(cudaEventRecord(*a, stream_of(ctx, d)));
+  return HDA_OK;
+}
+static int timed_end(hda_ctx_t* ctx, int d, int kind, cudaEvent_t a) {
+  if (!a) return HDA_OK;
+  cudaEvent_t b = get_event(ctx);
+  CK(cudaEventRecord(b, stream_of(ctx, d)));
+  ctx->tev.push_back(TimedEv{kind, a, b});
+  return HDA_OK;
+}
+
+static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k) {
+  if (t->msgs.empty()) return HDA_OK;
+  ExecPlan* ep;
+  ExecPlan scratch;
+  if (ctx->cache_on) {
+    auto it = ctx->exec.find(t->serial);
+    if (it == ctx->exec.end() || it->second.staged != (ctx->transport == HDA_XPORT_STAGED)) {
+      ExecPlan np;
+      int rc = build_exec(ctx, t, np);
+      if (rc) return rc;
+      ctx->exec[t->serial] = std::move(np);
+      it = ctx->exec.find(t->serial);
+    }
+    ep = &it->second;
+  } else {
+    int rc = build_exec(ctx, t, scratch);
+    if (rc) return rc;
+    ep = &scratch;
+  }
+  if (!ep->staged) {
+    for (PullJob& job : ep->pulls) {
+      const int q = job.dst;
+      CK(cudaSetDevice(ordinal_of(ctx, q)));
+      WaitList wl;
+      wl.n = 0;
+      SignalList sl;
+      sl.n = 0;
+      sl.val = k;
+      for (int p : job.srcs)
+        if (!same_stream(ctx, p, q)) {
+          wl_add(wl, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
+          sl.ptr[sl.n++] = ctx->dev[p].sync + SW_ACK + q;
+        }
+      int rc = launch_waits(ctx, q, wl);
+      if (rc) return rc;
+      cudaEvent_t a;
+      if ((rc = timed_begin(ctx, q, &a))) return rc;
+      for (const RunBatch& b : job.batches) {
+        CK(launch_copy_runs(b, stream_of(ctx, q)));
+        count_launch(ctx);
+      }
+      if ((rc = timed_end(ctx, q, -100, a))) return rc;
+      if ((rc = launch_signals(ctx, q, sl))) return rc;
+      for (auto& pr : job.pend) ctx->pend[pr.first][pr.second][q] = k;
+    }
+    return HDA_OK;
+  }
+  // STAGED
+  for (PackJob& job : ep->packs) {
+    const int p = job.src;
+    CK(cudaSetDevice(ordinal_of(ctx, p)));
+    WaitList wl;
+    wl.n = 0;
+    for (auto& e : ctx->stage_pend[p])
+      if (!same_stream(ctx, p, e.first)) wl_add(wl, ctx->dev[p].sync + SW_ACK + e.first, e.second);
+    ctx->stage_pend[p].clear();
+    int rc = launch_waits(ctx, p, wl);
+    if (rc) return rc;
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, p, &a))) return rc;
+    for (const RunBatch& b : job.batches) {
+      CK(launch_copy_runs(b, stream_of(ctx, p)));
+      count_launch(ctx);
+    }
+    if ((rc = timed_end(ctx, p, -100, a))) return rc;
+    SignalList sl;
+    sl.n = 0;
+    sl.val = k;
+    for (int q : job.dsts)
+      if (!same_stream(ctx, p, q)) sl.ptr[sl.n++] = ctx->dev[q].sync + SW_PACK + p;
+    if ((rc = launch_signals(ctx, p, sl))) return rc;
+  }
+  for (RecvJob& job : ep->recvs) {
+    const int q = job.dst;
+    CK(cudaSetDevice(ordinal_of(ctx, q)));
+    WaitList wl;
+    wl.n = 0;
+    SignalList sl;
+    sl.n = 0;
+    sl.val = k;
+    for (int p : job.srcs)
+      if (!same_stream(ctx, p, q)) {
+        wl_add(wl, ctx->dev[q].sync + SW_PACK + p, k);
+        sl.ptr[sl.n++] = ctx->dev[p].sync + SW_ACK + q;
+      }
+    int rc = launch_waits(ctx, q, wl);
+    if (rc) return rc;
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, q, &a))) return rc;
+    for (const Seg& s : job.segs)
+      CK(cudaMemcpyAsync(ctx->recv_stage[q] + s.dst_off, ctx->send_stage[s.src] + s.src_off, s.bytes,
+                         cudaMemcpyDeviceToDevice, stream_of(ctx, q)));
+    for (const RunBatch& b : job.unpack) {
+      CK(launch_copy_runs(b, stream_of(ctx, q)));
+      count_launch(ctx);
+    }
+    if ((rc = timed_end(ctx, q, -100, a))) return rc;
+    if ((rc = launch_signals(ctx, q, sl))) return rc;
+    for (int p : job.srcs) ctx->stage_pend[p].push_back({q, k});
+  }
+  return HDA_OK;
+}
+
+// WAR before device q overwrites cells of the arrays it defines
+static int war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q) {
+  WaitList wl;
+  wl.n = 0;
+  for (size_t i = 0; i < ci.arrays.size(); i++) {
+    if (ci.ldef[i][q].empty()) continue;
+    auto& row = ctx->pend[ci.arrays[i]][q];
+    for (int r = 0; r < ctx->P; r++) {
+      if (row[r] && !same_stream(ctx, q, r)) wl_add(wl, ctx->dev[q].sync + SW_ACK + r, row[r]);
+      row[r] = 0;
+    }
+  }
+  return launch_waits(ctx, q, wl);
+}
+
+static int signal_prod(hda_ctx_t* ctx, int q, unsigned long long k) {
+  SignalList sl;
+  sl.n = 0;
+  sl.val = k;
+  for (int r = 0; r < ctx->P; r++)
+    if (r != q && !same_stream(ctx, q, r)) sl.ptr[sl.n++] = ctx->dev[r].sync + SW_PROD + q;
+  return launch_signals(ctx, q, sl);
+}
+
+static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars) {
+  const CallInfo& ci = *t->info;
+  const TPart& pt = ctx->tr->part(ci.part);
+  const int X0 = ci.param_array[0];
+  const TArray& a0 = ctx->tr->array(X0);
+  int64_t S[3];
+  front_shape(a0.ndim, a0.shape, S);
+  const Box fb = front_box(a0.ndim, pt.box[q]);
+  cudaStream_t s = stream_of(ctx, q);
+  auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
+  switch (ci.kernel) {
+    case KN_JACOBI5:
+      CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, s));
+      break;
+    case KN_STENCIL9:
+      CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, s));
+      break;
+    case KN_STENCIL7_3D:
+      CK(launch_stencil7(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, s));
+      break;
+    case KN_COPY: {
+      RunDesc d = rect_desc(S, fb, a0.es);
+      d.src = P_(1);
+      d.dst = P_(0);
+      std::vector<RunDesc> v{d};
+      std::vector<RunBatch> bs;
+      batch_descs(v, bs);
+      for (auto& b : bs) CK(launch_copy_runs(b, s));
+      break;
+    }
+    case KN_SCALE:
+      CK(launch_scale(a0.dtype, P_(0), S, fb.lb, fb.ub, scalars[0], s));
+      break;
+    case KN_STAMP: {
+      const Rects& D = ci.ldef[0][q];
+      for (size_t i = 0; i < D.size(); i += 16) {
+        BoxList bl;
+        bl.n = 0;
+        for (size_t j = i; j < D.size() && j < i + 16; j++) {
+          Box b = front_box(a0.ndim, D[j]);
+          for (int k = 0; k < 3; k++) {
+            bl.lb[bl.n][k] = b.lb[k];
+            bl.ub[bl.n][k] = b.ub[k];
+          }
+          bl.n++;
+        }
+        CK(launch_stamp((int)a0.es, P_(0), S, bl, (unsigned long long)scalars[0], s));
+      }
+      break;
+    }
+    case KN_GEMM: {
+      const TArray& A = ctx->tr->array(ci.param_array[1]);
+      const TArray& B = ctx->tr->array(ci.param_array[2]);
+      CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], A.shape[1], fb.lb, fb.ub,
+                     (float)scalars[0], (float)scalars[1], s));
+      break;
+    }
+    default:
+      break;
+  }
+  count_launch(ctx);
+  return HDA_OK;
+}
+
+static void record_plan(hda_ctx_t* ctx, const Transition* t, bool hit, double us) {
+  ctx->last_plan.clear();
+  for (const Msg& m : t->msgs) {
+    hda_msg_t o;
+    o.array = m.array;
+    o.src = m.src;
+    o.dst = m.dst;
+    o.ndim = ctx->tr->array(m.array).ndim;
+    for (int k = 0; k < 3; k++) {
+      o.lb[k] = m.box.lb[k];
+      o.ub[k] = m.box.ub[k];
+    }
+    ctx->last_plan.push_back(o);
+  }
+  ctx->stats.n_apply++;
+  if (hit)
+    ctx->stats.plan_hits++;
+  else
+    ctx->stats.plan_misses++;
+  ctx->stats.last_msgs = (int64_t)t->msgs.size();
+  ctx->stats.last_bytes = t->bytes;
+  ctx->stats.msgs_total += (int64_t)t->msgs.size();
+  ctx->stats.bytes_total += t->bytes;
+  ctx->stats.tracker_us += us;
+}
+
+static bool arrays_ready(hda_ctx_t* ctx, const CallInfo& ci) {
+  if (ctx->plan_only) return true;
+  if (!ctx->sync_imported) return false;
+  for (int X : ci.arrays)
+    if (!ctx->arr[X].imported) return false;
+  return true;
+}
+
+using clk = std::chrono::steady_clock;
+
+// the full per-call pipeline shared by apply / read / write
+static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn* acc, int32_t n_acc,
+                const double* scalars, int32_t n_scalars, const void* host_in, void* host_out) {
+  auto t0 = clk::now();
+  const Transition* t = nullptr;
+  bool hit = false;
+  std::string err;
+  int rc = ctx->tr->plan(kernel, part, acc, n_acc, scalars, n_scalars, ctx->cache_on, &t, &hit, err);
+  if (rc) return fail(ctx, rc, err);
+  double us = std::chrono::duration<double, std::micro>(clk::now() - t0).count();
+  const CallInfo& ci = *t->info;
+  if (!arrays_ready(ctx, ci)) return fail(ctx, HDA_ESTATE, "SPMD handles not imported for an array");
+  const unsigned long long k = ++ctx->epoch;
+  if (!ctx->plan_only) {
+    DevGuard g(true);
+    if ((rc = do_exchange(ctx, t, k))) return rc;
+    const TPart& pt = ctx->tr->part(part);
+    for (int q = 0; q < ctx->P; q++) {
+      if (!ctx->dev[q].local) continue;
+      bool defines = false;
+      for (size_t i = 0; i < ci.arrays.size(); i++)
+        if (!ci.ldef[i][q].empty()) defines = true;
+      const bool has_work = !box_empty(pt.box[q]);
+      const bool kern = kernel > KN_NONE && (kernel == KN_STAMP ? defines : has_work);
+      const bool io = (kernel == KN_WRITE && has_work) || (kernel == KN_READ && has_work);
+      if (!defines && !kern && !io) continue;
+      CK(cudaSetDevice(ordinal_of(ctx, q)));
+      if (defines && (rc = war_waits(ctx, ci, q))) return rc;
+      const int X0 = ci.param_array[0];
+      const TArray& a0 = ctx->tr->array(X0);
+      if (io) {
+        int64_t S[3];
+        front_shape(a0.ndim, a0.shape, S);
+        Box fb = front_box(a0.ndim, pt.box[q]);
+        cudaMemcpy3DParms p;
+        std::memset(&p, 0, sizeof p);
+        const size_t es = a0.es;
+        void* host = kernel == KN_WRITE ? const_cast<void*>(host_in) : host_out;
+        cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)S[2] * es, (size_t)S[2], (size_t)S[1]);
+        cudaPitchedPtr dp = make_cudaPitchedPtr(ctx->arr[X0].ptr[q], (size_t)S[2] * es, (size_t)S[2], (size_t)S[1]);
+        cudaPos pos = make_cudaPos((size_t)fb.lb[2] * es, (size_t)fb.lb[1], (size_t)fb.lb[0]);
+        p.extent = make_cudaExtent((size_t)(fb.ub[2] - fb.lb[2]) * es, (size_t)(fb.ub[1] - fb.lb[1]),
+                                   (size_t)(fb.ub[0] - fb.lb[0]));
+        if (kernel == KN_WRITE) {
+          p.srcPtr = hp;
+          p.srcPos = pos;
+          p.dstPtr = dp;
+          p.dstPos = pos;
+          p.kind = cudaMemcpyHostToDevice;
+        } else {
+          p.srcPtr = dp;
+          p.srcPos = pos;
+          p.dstPtr = hp;
+          p.dstPos = pos;
+          p.kind = cudaMemcpyDeviceToHost;
+        }
+        if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
+      } else if (kern) {
+        cudaEvent_t a;
+        if ((rc = timed_begin(ctx, q, &a))) return rc;
+        if ((rc = run_kernel(ctx, t, q, scalars))) return rc;
+        if ((rc = timed_end(ctx, q, kernel, a))) return rc;
+      }
+      if (defines && (rc = signal_prod(ctx, q, k))) return rc;
+    }
+  }
+  // every rank knows every device's definitions (SPMD replicated tracker)
+  for (int q = 0; q < ctx->P; q++)
+    for (size_t i = 0; i < ci.arrays.size(); i++)
+      if (!ci.ldef[i][q].empty()) ctx->last_prod[q] = k;
+  auto t1 = clk::now();
+  ctx->tr->commit(t);
+  us += std::chrono::duration<double, std::micro>(clk::now() - t1).count();
+  record_plan(ctx, t, hit, us);
+  if (!ctx->plan_only && (kernel == KN_WRITE || kernel == KN_READ)) {
+    DevGuard g(true);
+    if ((rc = sync_all(ctx))) return rc;
+  }
+  return HDA_OK;
+}
+
+// ====================================================================== C-ABI
+
+static hda_ctx_t* new_ctx(int P) {
+  hda_ctx_t* ctx = new hda_ctx_t();
+  ctx->P = P;
+  ctx->tr = std::make_unique<Tracker>(P);
+  ctx->dev.assign(P, Dev());
+  ctx->last_prod.assign(P, 0);
+  ctx->stage_pend.assign(P, {});
+  ctx->send_stage.assign(P, nullptr);
+  ctx->recv_stage.assign(P, nullptr);
+  ctx->send_cap.assign(P, 0);
+  ctx->recv_cap.assign(P, 0);
+  return ctx;
+}
+
+static int setup_gpu_common(hda_ctx_t* ctx) {
+  for (auto& g : ctx->gpus) {
+    CK(cudaSetDevice(g.ordinal));
+    CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  }
+  CK(cudaHostAlloc((void**)&ctx->err_host, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+  *ctx->err_host = 0;
+  for (int d = 0; d < ctx->P; d++) {
+    if (!ctx->dev[d].local) continue;
+    CK(cudaSetDevice(ordinal_of(ctx, d)));
+    CK(cudaMalloc((void**)&ctx->dev[d].sync, SW_WORDS * sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->dev[d].sync, 0, SW_WORDS * sizeof(unsigned long long)));
+    ctx->dev[d].sync_alloc = true;
+  }
+  CK(cudaDeviceSynchronize());
+  return HDA_OK;
+}
+
+extern "C" {
+
+const char* hda_version(void) { return "hdarray-b200 0.1 (sm_100a)"; }
+
+int hda_init(hda_ctx_t** out, int32_t n_gpus, const int32_t* gpu_ids, int32_t n_devices) {
+  if (!out) return HDA_EINVAL;
+  *out = nullptr;
+  if (n_devices < 1 || n_devices > HDA_MAX_DEVICES || n_gpus < 0 || n_gpus > n_devices) return HDA_EINVAL;
+  hda_ctx_t* ctx = new_ctx(n_devices);
+  ctx->plan_only = n_gpus == 0;
+  for (int d = 0; d < n_devices; d++) ctx->dev[d].local = true;
+  if (!ctx->plan_only) {
+    DevGuard g(true);
+    for (int i = 0; i < n_gpus; i++) ctx->gpus.push_back(Gpu{gpu_ids ? gpu_ids[i] : i, nullptr});
+    for (int d = 0; d < n_devices; d++) ctx->dev[d].gpu = d % n_gpus;
+    for (int i = 0; i < n_gpus; i++) {
+      cudaError_t e = cudaSetDevice(ctx->gpus[i].ordinal);
+      if (e != cudaSuccess) {
+        *out = ctx;
+        return cuda_fail(ctx, e, "cudaSetDevice");
+      }
+      for (int j = 0; j < n_gpus; j++) {
+        if (i == j || ctx->gpus[i].ordinal == ctx->gpus[j].ordinal) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, ctx->gpus[i].ordinal, ctx->gpus[j].ordinal);
+        if (!can) {
+          *out = ctx;
+          return fail(ctx, HDA_EUNSUPPORTED, "GPUs without peer access");
+        }
+        e = cudaDeviceEnablePeerAccess(ctx->gpus[j].ordinal, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) {
+          *out = ctx;
+          return cuda_fail(ctx, e, "cudaDeviceEnablePeerAccess");
+        }
+      }
+    }
+    int rc = setup_gpu_common(ctx);
+    if (rc) {
+      *out = ctx;
+      return rc;
+    }
+  }
+  *out = ctx;
+  return HDA_OK;
+}
+
+int hda_init_spmd(hda_ctx_t** out, int32_t n_devices, int32_t rank, int32_t gpu_id) {
+  if (!out) return HDA_EINVAL;
+  *out = nullptr;
+  if (n_devices < 1 || n_devices > HDA_MAX_DEVICES || rank < 0 || rank >= n_devices) return HDA_EINVAL;
+  hda_ctx_t* ctx = new_ctx(n_devices);
+  ctx->spmd = true;
+  ctx->rank = rank;
+  ctx->plan_only = gpu_id < 0;
+  ctx->dev[rank].local = true;
+  if (ctx->plan_only) {
+    for (int d = 0; d < n_devices; d++) ctx->dev[d].local = d == rank;
+  } else {
+    DevGuard g(true);
+    ctx->gpus.push_back(Gpu{gpu_id, nullptr});
+    ctx->dev[rank].gpu = 0;
+    ctx->sync_imported = n_devices == 1;
+    int rc = setup_gpu_common(ctx);
+    *out = ctx;
+    return rc;
+  }
+  *out = ctx;
+  return HDA_OK;
+}
+
+int hda_finalize(hda_ctx_t* ctx) {
+  if (!ctx) return HDA_EINVAL;
+  if (!ctx->plan_only) {
+    DevGuard g(true);
+    for (auto& gp : ctx->gpus) {
+      cudaSetDevice(gp.ordinal);
+      cudaStreamSynchronize(gp.stream);
+    }
+    for (size_t X = 0; X < ctx->arr.size(); X++)
+      for (int d = 0; d < ctx->P; d++) {
+        if (ctx->arr[X].alloc.size() && ctx->arr[X].alloc[d]) {
+          cudaSetDevice(ordinal_of(ctx, d));
+          cudaFree(ctx->arr[X].ptr[d]);
+        } else if (ctx->arr[X].ipc.size() && ctx->arr[X].ipc[d]) {
+          cudaIpcCloseMemHandle(ctx->arr[X].ptr[d]);
+        }
+      }
+    for (int d = 0; d < ctx->P; d++) {
+      if (ctx->dev[d].sync_alloc) {
+        cudaSetDevice(ordinal_of(ctx, d));
+        cudaFree(ctx->dev[d].sync);
+      } else if (ctx->dev[d].sync_ipc) {
+        cudaIpcCloseMemHandle(ctx->dev[d].sync);
+      }
+      if (ctx->send_stage[d]) cudaFree(ctx->send_stage[d]);
+      if (ctx->recv_stage[d]) cudaFree(ctx->recv_stage[d]);
+    }
+    for (auto& e : ctx->tev) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (auto& gp : ctx->gpus) {
+      cudaSetDevice(gp.ordinal);
+      cudaStreamDestroy(gp.stream);
+    }
+    if (ctx->err_host) cudaFreeHost(ctx->err_host);
+  }
+  delete ctx;
+  return HDA_OK;
+}
+
+int hda_num_devices(const hda_ctx_t* ctx, int32_t* n) {
+  if (!ctx || !n) return HDA_EINVAL;
+  *n = ctx->P;
+  return HDA_OK;
+}
+
+int hda_is_local(const hda_ctx_t* ctx, int32_t dev, int32_t* is_local) {
+  if (!ctx || !is_local || dev < 0 || dev >= ctx->P) return HDA_EINVAL;
+  *is_local = ctx->dev[dev].local ? 1 : 0;
+  return HDA_OK;
+}
+
+int hda_spmd_export(hda_ctx_t* ctx, hda_array_t arr, void* out) {
+  GUARD();
+  if (!out) return fail(ctx, HDA_EINVAL, "null blob");
+  std::memset(out, 0, HDA_HANDLE_BYTES);
+  if (!ctx->spmd || ctx->plan_only) return HDA_OK;
+  char* base;
+  if (arr == -1) {
+    base = (char*)ctx->dev[ctx->rank].sync;
+  } else {
+    if (!ctx->tr->array_ok(arr)) return fail(ctx, HDA_EINVAL, "unknown array");
+    base = ctx->arr[arr].ptr[ctx->rank];
+  }
+  DevGuard g(true);
+  CK(cudaSetDevice(ctx->gpus[0].ordinal));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, base));
+  uint32_t hdr[2] = {BLOB_MAGIC, (uint32_t)ctx->rank};
+  std::memcpy(out, hdr, 8);
+  std::memcpy((char*)out + 8, &h, sizeof h);
+  return HDA_OK;
+}
+
+int hda_spmd_import(hda_ctx_t* ctx, hda_array_t arr, const void* all) {
+  GUARD();
+  if (!all) return fail(ctx, HDA_EINVAL, "null blobs");
+  if (!ctx->spmd || ctx->plan_only) return HDA_OK;
+  if (arr != -1 && !ctx->tr->array_ok(arr)) return fail(ctx, HDA_EINVAL, "unknown array");
+  DevGuard g(true);
+  CK(cudaSetDevice(ctx->gpus[0].ordinal));
+  for (int p = 0; p < ctx->P; p++) {
+    if (p == ctx->rank) continue;
+    const char* b = (const char*)all + (size_t)p * HDA_HANDLE_BYTES;
+    uint32_t hdr[2];
+    std::memcpy(hdr, b, 8);
+    if (hdr[0] != BLOB_MAGIC || (int)hdr[1] != p) return fail(ctx, HDA_EINVAL, "bad SPMD blob");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, b + 8, sizeof h);
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    if (arr == -1) {
+      ctx->dev[p].sync = (unsigned long long*)ptr;
+      ctx->dev[p].sync_ipc = true;
+    } else {
+      ctx->arr[arr].ptr[p] = (char*)ptr;
+      ctx->arr[arr].ipc[p] = 1;
+    }
+  }
+  if (arr == -1)
+    ctx->sync_imported = true;
+  else
+    ctx->arr[arr].imported = true;
+  return HDA_OK;
+}
+
+static int create_common(hda_ctx_t* ctx, int32_t dtype, int32_t ndim, const int64_t* shape, hda_array_t* out,
+                         int* id_out) {
+  if (!shape || !out) return fail(ctx, HDA_EINVAL, "null argument");
+  std::string err;
+  int id = ctx->tr->add_array(dtype, ndim, shape, err);
+  if (id < 0) return fail(ctx, id, err);
+  ArrRT a;
+  a.ptr.assign(ctx->P, nullptr);
+  a.alloc.assign(ctx->P, 0);
+  a.ipc.assign(ctx->P, 0);
+  const TArray& t = ctx->tr->array(id);
+  a.bytes = (size_t)(t.shape[0] * t.shape[1] * t.shape[2]) * t.es;
+  a.imported = !ctx->spmd || ctx->P == 1 || ctx->plan_only;
+  ctx->arr.push_back(a);
+  ctx->pend.emplace_back(ctx->P, std::vector<unsigned long long>(ctx->P, 0));
+  *id_out = id;
+  return HDA_OK;
+}
+
+int hda_create(hda_ctx_t* ctx, int32_t dtype, int32_t ndim, const int64_t* shape, const void* init_host,
+               hda_array_t* out) {
+  GUARD();
+  int id;
+  int rc = create_common(ctx, dtype, ndim, shape, out, &id);
+  if (rc) return rc;
+  if (!ctx->plan_only) {
+    DevGuard g(true);
+    ArrRT& a = ctx->arr[id];
+    for (int d = 0; d < ctx->P; d++) {
+      if (!ctx->dev[d].local) continue;
+      CK(cudaSetDevice(ordinal_of(ctx, d)));
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, a.bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, HDA_ENOMEM, "cudaMalloc of a replica failed");
+      }
+      a.ptr[d] = (char*)p;
+      a.alloc[d] = 1;
+      if (init_host)
+        CK(cudaMemcpy(p, init_host, a.bytes, cudaMemcpyHostToDevice));
+      else
+        CK(cudaMemset(p, 0, a.bytes));
+    }
+    CK(cudaDeviceSynchronize());
+  }
+  *out = id;
+  return HDA_OK;
+}
+
+int hda_create_ext(hda_ctx_t* ctx, int32_t dtype, int32_t ndim, const int64_t* shape, void* const* dev_ptrs,
+                   hda_array_t* out) {
+  GUARD();
+  if (ctx->spmd) return fail(ctx, HDA_EUNSUPPORTED, "hda_create_ext is single-process only");
+  if (!dev_ptrs && !ctx->plan_only) return fail(ctx, HDA_EINVAL, "null device pointers");
+  int id;
+  int rc = create_common(ctx, dtype, ndim, shape, out, &id);
+  if (rc) return rc;
+  if (!ctx->plan_only)
+    for (int d = 0; d < ctx->P; d++) ctx->arr[id].ptr[d] = (char*)dev_ptrs[d];
+  *out = id;
+  return HDA_OK;
+}
+
+int hda_free(hda_ctx_t* ctx, hda_array_t arr) {
+  GUARD();
+  if (!ctx->tr->array_ok(arr)) return fail(ctx, HDA_EINVAL, "unknown array");
+  if (!ctx->plan_only) {
+    DevGuard g(true);
+    int rc = sync_all(ctx);
+    if (rc) return rc;
+    ArrRT& a = ctx->arr[arr];
+    for (int d = 0; d < ctx->P; d++) {
+      if (a.alloc[d]) {
+        CK(cudaSetDevice(ordinal_of(ctx, d)));
+        CK(cudaFree(a.ptr[d]));
+      } else if (a.ipc[d]) {
+        CK(cudaIpcCloseMemHandle(a.ptr[d]));
+      }
+      a.ptr[d] = nullptr;
+      a.alloc[d] = a.ipc[d] = 0;
+    }
+  }
+  ctx->tr->free_array(arr);
+  ctx->exec.clear();
+  return HDA_OK;
+}
+
+int hda_device_ptr(hda_ctx_t* ctx, hda_array_t arr, int32_t dev, void** out) {
+  GUARD();
+  if (!out || !ctx->tr->array_ok(arr) || dev < 0 || dev >= ctx->P) return fail(ctx, HDA_EINVAL, "bad argument");
+  *out = ctx->arr[arr].ptr[dev];
+  return HDA_OK;
+}
+
+int hda_partition(hda_ctx_t* ctx, int32_t kind, int32_t ndim, const int64_t* domain, const int64_t* lb,
+                  const int64_t* ub, hda_part_t* out) {
+  GUARD();
+  if (!domain || !lb || !ub || !out) return fail(ctx, HDA_EINVAL, "null argument");
+  std::string err;
+  int id = ctx->tr->add_partition(kind, ndim, domain, lb, ub, err);
+  if (id < 0) return fail(ctx, id, err);
+  *out = id;
+  return HDA_OK;
+}
+
+int hda_partition_manual(hda_ctx_t* ctx, int32_t ndim, const int64_t* domain, const int64_t* lbs,
+                         const int64_t* ubs, hda_part_t* out) {
+  GUARD();
+  if (!domain || !lbs || !ubs || !out) return fail(ctx, HDA_EINVAL, "null argument");
+  std::string err;
+  int id = ctx->tr->add_partition_manual(ndim, domain, lbs, ubs, err);
+  if (id < 0) return fail(ctx, id, err);
+  *out = id;
+  return HDA_OK;
+}
+
+int hda_partition_region(const hda_ctx_t* ctx, hda_part_t part, int32_t dev, int64_t* lb, int64_t* ub) {
+  if (!ctx || !lb || !ub || !ctx->tr->part_ok(part) || dev < 0 || dev >= ctx->P) return HDA_EINVAL;
+  const TPart& p = ctx->tr->part(part);
+  for (int k = 0; k < p.ndim; k++) {
+    lb[k] = p.box[dev].lb[k];
+    ub[k] = p.box[dev].ub[k];
+  }
+  return HDA_OK;
+}
+
+int hda_apply(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const hda_access_t* acc, int32_t n_acc,
+              const double* scalars, int32_t n_scalars) {
+  GUARD();
+  if (kernel < 0 || kernel >= KN_COUNT) return fail(ctx, HDA_EINVAL, "unknown kernel");
+  if (n_acc < 0 || n_acc > 64 || (n_acc && !acc)) return fail(ctx, HDA_EINVAL, "bad access list");
+  if (n_scalars < 0 || (n_scalars && !scalars)) return fail(ctx, HDA_EINVAL, "bad scalars");
+  AccessIn in[64];
+  for (int i = 0; i < n_acc; i++) in[i] = AccessIn{acc[i].array, acc[i].n_use, acc[i].use, acc[i].n_def, acc[i].def};
+  return call(ctx, kernel, part, in, n_acc, scalars, n_scalars, nullptr, nullptr);
+}
+
+int hda_sync(hda_ctx_t* ctx) {
+  GUARD();
+  if (ctx->plan_only) return HDA_OK;
+  DevGuard g(true);
+  return sync_all(ctx);
+}
+
+int hda_write(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, const void* host_full) {
+  GUARD();
+  if (!ctx->tr->array_ok(arr)) return fail(ctx, HDA_EINVAL, "unknown array");
+  if (!host_full && !ctx->plan_only) return fail(ctx, HDA_EINVAL, "null host buffer");
+  static const int32_t zero[3] = {0, 0, 0};
+  AccessIn in{arr, 0, nullptr, 1, zero};
+  return call(ctx, KN_WRITE, part, &in, 1, nullptr, 0, host_full, nullptr);
+}
+
+int hda_read(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, void* host_full) {
+  GUARD();
+  if (!ctx->tr->array_ok(arr)) return fail(ctx, HDA_EINVAL, "unknown array");
+  static const int32_t zero[3] = {0, 0, 0};
+  AccessIn in{arr, 1, zero, 0, nullptr};
+  return call(ctx, KN_READ, part, &in, 1, nullptr, 0, nullptr, host_full);
+}
+
+int hda_set_transport(hda_ctx_t* ctx, int32_t transport) {
+  GUARD();
+  if (transport != HDA_XPORT_FUSED && transport != HDA_XPORT_STAGED) return fail(ctx, HDA_EINVAL, "transport");
+  if (transport == HDA_XPORT_STAGED && ctx->spmd && ctx->P > 1)
+    return fail(ctx, HDA_EUNSUPPORTED, "staged transport is single-process only");
+  ctx->transport = transport;
+  return HDA_OK;
+}
+
+int hda_set_plan_cache(hda_ctx_t* ctx, int32_t enabled) {
+  GUARD();
+  ctx->cache_on = enabled != 0;
+  return HDA_OK;
+}
+
+int hda_set_kernel_timing(hda_ctx_t* ctx, int32_t enabled) {
+  GUARD();
+  ctx->ktiming = enabled != 0 && !ctx->plan_only;
+  return HDA_OK;
+}
+
+static int drain_timing(hda_ctx_t* ctx) {
+  if (ctx->tev.empty()) return HDA_OK;
+  DevGuard g(true);
+  int rc = sync_all(ctx);
+  if (rc) return rc;
+  for (auto& e : ctx->tev) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e.a, e.b));
+    if (e.kind == -100) {
+      ctx->xtime_ms += ms;
+      ctx->xcount++;
+    } else if (e.kind >= 0 && e.kind < KN_COUNT) {
+      ctx->ktime_ms[e.kind] += ms;
+      ctx->kcount[e.kind]++;
+    }
+    ctx->ev_pool.push_back(e.a);
+    ctx->ev_pool.push_back(e.b);
+  }
+  ctx->tev.clear();
+  return HDA_OK;
+}
+
+int hda_kernel_time(hda_ctx_t* ctx, int32_t kernel, double* total_ms, int64_t* launches) {
+  GUARD();
+  if (kernel < 0 || kernel >= KN_COUNT || !total_ms || !launches) return fail(ctx, HDA_EINVAL, "bad argument");
+  int rc = drain_timing(ctx);
+  if (rc) return rc;
+  *total_ms = ctx->ktime_ms[kernel];
+  *launches = ctx->kcount[kernel];
+  return HDA_OK;
+}
+
+int hda_exchange_time(hda_ctx_t* ctx, double* total_ms, int64_t* n) {
+  GUARD();
+  if (!total_ms || !n) return fail(ctx, HDA_EINVAL, "bad argument");
+  int rc = drain_timing(ctx);
+  if (rc) return rc;
+  *total_ms = ctx->xtime_ms;
+  *n = ctx->xcount;
+  return HDA_OK;
+}
+
+int hda_stream(hda_ctx_t* ctx, int32_t dev, void** stream) {
+  GUARD();
+  if (!stream || dev < 0 || dev >= ctx->P || !ctx->dev[dev].local || ctx->plan_only)
+    return fail(ctx, HDA_EINVAL, "no stream for that device");
+  *stream = (void*)stream_of(ctx, dev);
+  return HDA_OK;
+}
+
+int hda_last_plan(const hda_ctx_t* ctx, hda_msg_t* out, int32_t cap, int32_t* n_out) {
+  if (!ctx || !n_out) return HDA_EINVAL;
+  *n_out = (int32_t)ctx->last_plan.size();
+  if (out)
+    for (int32_t i = 0; i < cap && i < *n_out; i++) out[i] = ctx->last_plan[i];
+  return HDA_OK;
+}
+
+int hda_owner_map(const hda_ctx_t* ctx, hda_array_t arr, int8_t* out) {
+  if (!ctx || !out || !ctx->tr->array_ok(arr)) return HDA_EINVAL;
+  ctx->tr->owner_map(arr, out);
+  return HDA_OK;
+}
+
+int hda_read_replica(hda_ctx_t* ctx, hda_array_t arr, int32_t dev, void* host_full) {
+  GUARD();
+  if (!ctx->tr->array_ok(arr) || !host_full || dev < 0 || dev >= ctx->P || !ctx->dev[dev].local || ctx->plan_only)
+    return fail(ctx, HDA_EINVAL, "bad argument");
+  DevGuard g(true);
+  int rc = sync_all(ctx);
+  if (rc) return rc;
+  CK(cudaSetDevice(ordinal_of(ctx, dev)));
+  CK(cudaMemcpy(host_full, ctx->arr[arr].ptr[dev], ctx->arr[arr].bytes, cudaMemcpyDeviceToHost));
+  return HDA_OK;
+}
+
+int hda_stats(const hda_ctx_t* ctx, hda_stats_t* out) {
+  if (!ctx || !out) return HDA_EINVAL;
+  *out = ctx->stats;
+  return HDA_OK;
+}
+
+int hda_reset_stats(hda_ctx_t* ctx) {
+  if (!ctx) return HDA_EINVAL;
+  int rc = drain_timing(ctx);
+  ctx->stats = hda_stats_t{};
+  for (int k = 0; k < KN_COUNT; k++) {
+    ctx->ktime_ms[k] = 0;
+    ctx->kcount[k] = 0;
+  }
+  ctx->xtime_ms = 0;
+  ctx->xcount = 0;
+  return rc;
+}
+
+const char* hda_last_error(const hda_ctx_t* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

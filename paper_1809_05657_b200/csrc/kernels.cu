@@ -1,0 +1,556 @@
+// kernels.cu — sm_100a kernels of the exchange path and the user kernels.
+//
+//  copy_runs_kernel   strided-rect raw copy: fused pull (peer replica -> local replica
+//                     over NVLink = pack + transfer + unpack), pack, unpack, COPY
+//  wait / signal      cross-device ordering words (spin with timeout / release store)
+//  jacobi5            P:L459 A = (((W+E)+N)+S) * 0.25
+//  stencil9           reading R12: (4*(((W+E)+N)+S) + (((NW+NE)+SW)+SE)) / 20
+//  stencil7           reading R13: (((((x-+x+)+y-)+y+)+z-)+z+) / 6
+//  scale, stamp       elementwise helpers (repartition kernel, test kernel)
+//
+// Shapes/boxes passed to the user-kernel launchers are FRONT-padded to 3-D so that
+// dimension 2 is always the contiguous one.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+
+namespace hda {
+
+// =====================================================================================
+// strided rectangle copy
+// =====================================================================================
+
+int64_t run_desc_units(RunDesc& d) {
+  int64_t runs = (int64_t)d.n0 * d.n1;
+  if (runs == 0 || d.run_bytes == 0) {
+    d.chunks = 1;
+    return 0;
+  }
+  if (d.run_bytes <= 64) {
+    d.chunks = 0;
+    return (runs + 31) / 32;
+  }
+  d.chunks = (int32_t)((d.run_bytes + kChunkBytes - 1) / kChunkBytes);
+  return runs * d.chunks;
+}
+
+__device__ __forceinline__ void copy_elem(char* d, const char* s, int es) {
+  switch (es) {
+    case 8: *reinterpret_cast<unsigned long long*>(d) = *reinterpret_cast<const unsigned long long*>(s); break;
+    case 4: *reinterpret_cast<unsigned int*>(d) = *reinterpret_cast<const unsigned int*>(s); break;
+    case 2: *reinterpret_cast<unsigned short*>(d) = *reinterpret_cast<const unsigned short*>(s); break;
+    default: *d = *s;
+  }
+}
+
+// one warp moves n bytes; 16-byte vectors when src and dst share the 16-byte phase
+__device__ __forceinline__ void warp_copy(char* d, const char* s, int64_t n, int es, int lane) {
+  if ((((uintptr_t)s ^ (uintptr_t)d) & 15) == 0) {
+    int64_t head = (16 - ((uintptr_t)s & 15)) & 15;
+    if (head > n) head = n;
+    for (int64_t i = (int64_t)lane * es; i < head; i += 32 * es) copy_elem(d + i, s + i, es);
+    const uint4* s4 = reinterpret_cast<const uint4*>(s + head);
+    uint4* d4 = reinterpret_cast<uint4*>(d + head);
+    const int64_t nv = (n - head) >> 4;
+    int64_t i = lane;
+    for (; i + 96 < nv; i += 128) {  // four 16-byte loads in flight per lane
+      uint4 a = s4[i], b = s4[i + 32], c = s4[i + 64], e = s4[i + 96];
+      d4[i] = a;
+      d4[i + 32] = b;
+      d4[i + 64] = c;
+      d4[i + 96] = e;
+    }
+    for (; i < nv; i += 32) d4[i] = s4[i];
+    for (int64_t j = head + (nv << 4) + (int64_t)lane * es; j < n; j += 32 * es) copy_elem(d + j, s + j, es);
+  } else {
+    for (int64_t j = (int64_t)lane * es; j < n; j += 32 * es) copy_elem(d + j, s + j, es);
+  }
+}
+
+__global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ RunBatch b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < b.total_units; u += nwarps) {
+    int k = 0;
+    while (k + 1 < b.n && b.d[k + 1].unit_begin <= u) k++;
+    const RunDesc& d = b.d[k];
+    const int64_t lu = u - d.unit_begin;
+    if (d.chunks > 0) {
+      const int64_t run = lu / d.chunks, c = lu - run * d.chunks;
+      const int64_t i0 = run / d.n1, i1 = run - i0 * d.n1;
+      const char* s = d.src + d.src_off + i0 * d.src_p0 + i1 * d.src_p1;
+      char* t = d.dst + d.dst_off + i0 * d.dst_p0 + i1 * d.dst_p1;
+      const int64_t b0 = c * kChunkBytes;
+      const int64_t b1 = min(b0 + kChunkBytes, d.run_bytes);
+      warp_copy(t + b0, s + b0, b1 - b0, d.es, lane);
+    } else {
+      const int64_t run = lu * 32 + lane;
+      if (run < (int64_t)d.n0 * d.n1) {
+        const int64_t i0 = run / d.n1, i1 = run - i0 * d.n1;
+        const char* s = d.src + d.src_off + i0 * d.src_p0 + i1 * d.src_p1;
+        char* t = d.dst + d.dst_off + i0 * d.dst_p0 + i1 * d.dst_p1;
+        for (int64_t j = 0; j < d.run_bytes; j += d.es) copy_elem(t + j, s + j, d.es);
+      }
+    }
+  }
+}
+
+cudaError_t launch_copy_runs(const RunBatch& b, cudaStream_t s) {
+  if (b.total_units <= 0) return cudaSuccess;
+  int64_t blocks = (b.total_units + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  copy_runs_kernel<<<(unsigned)blocks, 256, 0, s>>>(b);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// cross-device ordering
+// =====================================================================================
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void wait_kernel(const __grid_constant__ WaitList w, int* err, long long timeout_ns) {
+  const int i = threadIdx.x;
+  if (i < w.n) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(w.ptr[i]) < w.val[i]) {
+      __nanosleep(100);
+      if ((long long)(globaltimer() - t0) > timeout_ns) {
+        *reinterpret_cast<volatile int*>(err) = -7;  // HDA_ETIMEOUT, host-mapped
+        __threadfence_system();
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void signal_kernel(const __grid_constant__ SignalList l) {
+  __threadfence_system();
+  const int i = threadIdx.x;
+  if (i < l.n) st_release_sys(l.ptr[i], l.val);
+}
+
+cudaError_t launch_wait(const WaitList& w, int* err_flag, long long timeout_ns, cudaStream_t s) {
+  if (w.n <= 0) return cudaSuccess;
+  wait_kernel<<<1, kMaxDev, 0, s>>>(w, err_flag, timeout_ns);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_signal(const SignalList& l, cudaStream_t s) {
+  if (l.n <= 0) return cudaSuccess;
+  signal_kernel<<<1, kMaxDev, 0, s>>>(l);
+  return cudaGetLastError();
+}
+
+// =====================================================================================
+// 2-D stencils: 16-byte column vectors per thread, marching down rows with a
+// register window; horizontal neighbours by warp shuffles (edge lanes load).
+// Every input element is fetched from DRAM once per block (2 halo rows per ROWS).
+// =====================================================================================
+
+template <typename T>
+struct V16;
+template <>
+struct V16<double> {
+  static constexpr int n = 2;
+  __device__ static void load(double (&r)[2], const double* p) {
+    double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    r[0] = v.x;
+    r[1] = v.y;
+  }
+  __device__ static void store(double* p, const double (&r)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(r[0], r[1]);
+  }
+};
+template <>
+struct V16<float> {
+  static constexpr int n = 4;
+  __device__ static void load(float (&r)[4], const float* p) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    r[0] = v.x;
+    r[1] = v.y;
+    r[2] = v.z;
+    r[3] = v.w;
+  }
+  __device__ static void store(float* p, const float (&r)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
+  }
+};
+
+constexpr int ST_THREADS = 128;  // threads per block along the row
+constexpr int ST_GROUP = 8;      // rows loaded together (loads in flight per thread)
+
+template <typename T>
+__device__ __forceinline__ T quarter(T x);
+template <>
+__device__ __forceinline__ double quarter(double x) { return x * 0.25; }
+template <>
+__device__ __forceinline__ float quarter(float x) { return x * 0.25f; }
+
+template <typename T>
+__device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
+  T a = ((w + e) + n) + s;
+  T c = ((nw + ne) + sw) + se;
+  T t = T(4) * a;
+  t = t + c;
+  return t / T(20);
+}
+
+// KIND 0 = JACOBI5, 1 = STENCIL9
+template <typename T, int KIND, int ROWS>
+__global__ void __launch_bounds__(ST_THREADS) stencil2d_kernel(const T* __restrict__ in,
+                                                             T* __restrict__ out, int64_t ld,
+                                                             int64_t r0, int64_t r1, int64_t c0,
+                                                             int64_t c1, int64_t cbase) {
+  constexpr int V = V16<T>::n;
+  constexpr int W = ST_GROUP + 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t col = cbase + ((int64_t)blockIdx.x * ST_THREADS + threadIdx.x) * V;
+  const bool live = col < ld;
+  const int64_t rs = r0 + (int64_t)blockIdx.y * ROWS;
+  const int64_t re = min(rs + (int64_t)ROWS, r1);
+  T w[W][V];
+  T lft[W], rgt[W];  // left neighbour of element 0, right neighbour of element V-1
+
+  auto load_row = [&](T(&r)[V], int64_t row) {
+    if (live) {
+      V16<T>::load(r, in + row * ld + col);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; v++) r[v] = T(0);
+    }
+  };
+  auto edges = [&](const T(&r)[V], int64_t row, T& L, T& R) {
+    L = __shfl_up_sync(0xffffffffu, r[V - 1], 1);
+    R = __shfl_down_sync(0xffffffffu, r[0], 1);
+    if (lane == 0 && live) L = __ldg(in + row * ld + col - 1);
+    if (lane == 31 && live) R = __ldg(in + row * ld + col + V);
+  };
+
+  load_row(w[0], rs - 1);
+  load_row(w[1], rs);
+  if (KIND == 1) {
+    edges(w[0], rs - 1, lft[0], rgt[0]);
+    edges(w[1], rs, lft[1], rgt[1]);
+  }
+  for (int64_t base = rs; base < re; base += ST_GROUP) {
+#pragma unroll
+    for (int k = 0; k < ST_GROUP; k++)
+      if (base + 1 + k <= re) load_row(w[k + 2], base + 1 + k);
+#pragma unroll
+    for (int k = 0; k < ST_GROUP; k++) {
+      const int64_t r = base + k;
+      if (r >= re) break;
+      T o[V];
+      if (KIND == 0) {
+        T L, R;
+        edges(w[k + 1], r, L, R);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+          const T left = v == 0 ? L : w[k + 1][v - 1];
+          const T right = v == V - 1 ? R : w[k + 1][v + 1];
+          o[v] = quarter<T>(((left + right) + w[k][v]) + w[k + 2][v]);
+        }
+      } else {
+        edges(w[k + 2], r + 1, lft[k + 2], rgt[k + 2]);
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+          const T* up = w[k];
+          const T* cu = w[k + 1];
+          const T* dn = w[k + 2];
+          const T cl = v == 0 ? lft[k + 1] : cu[v - 1], cr = v == V - 1 ? rgt[k + 1] : cu[v + 1];
+          const T ul = v == 0 ? lft[k] : up[v - 1], ur = v == V - 1 ? rgt[k] : up[v + 1];
+          const T dl = v == 0 ? lft[k + 2] : dn[v - 1], dr = v == V - 1 ? rgt[k + 2] : dn[v + 1];
+          o[v] = st9<T>(cl, cr, up[v], dn[v], ul, ur, dl, dr);
+        }
+      }
+      if (live) {
+        T* dst = out + r * ld + col;
+        if (col >= c0 && col + V <= c1) {
+          V16<T>::store(dst, o);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; v++)
+            if (col + v >= c0 && col + v < c1) dst[v] = o[v];
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      w[0][v] = w[ST_GROUP][v];
+      w[1][v] = w[ST_GROUP + 1][v];
+    }
+    if (KIND == 1) {
+      lft[0] = lft[ST_GROUP];
+      rgt[0] = rgt[ST_GROUP];
+      lft[1] = lft[ST_GROUP + 1];
+      rgt[1] = rgt[ST_GROUP + 1];
+    }
+  }
+}
+
+// scalar fallback for row pitches that are not 16-byte multiples (small test shapes)
+template <typename T, int KIND>
+__global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
+                                        int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = r0 + blockIdx.y;
+  if (c >= c1 || r >= r1) return;
+  const T* p = in + r * ld + c;
+  if (KIND == 0) {
+    out[r * ld + c] = quarter<T>(((p[-1] + p[1]) + p[-ld]) + p[ld]);
+  } else {
+    out[r * ld + c] = st9<T>(p[-1], p[1], p[-ld], p[ld], p[-ld - 1], p[-ld + 1], p[ld - 1], p[ld + 1]);
+  }
+}
+
+template <typename T, int KIND>
+static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* lb,
+                                      const int64_t* ub, cudaStream_t s) {
+  const int64_t ld = shape[2];
+  const int64_t r0 = lb[1], r1 = ub[1], c0 = lb[2], c1 = ub[2];
+  if (r0 >= r1 || c0 >= c1 || lb[0] >= ub[0]) return cudaSuccess;
+  constexpr int V = V16<T>::n;
+  const bool vec = (ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
+                   ((uintptr_t)out % 16) == 0;
+  if (vec) {
+    constexpr int ROWS = 32;
+    const int64_t cbase = c0 - (c0 % V);
+    const int64_t per_block = (int64_t)ST_THREADS * V;
+    dim3 grid((unsigned)((c1 - cbase + per_block - 1) / per_block), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));
+    stencil2d_kernel<T, KIND, ROWS><<<grid, ST_THREADS, 0, s>>>(in, out, ld, r0, r1, c0, c1, cbase);
+  } else {
+    dim3 grid((unsigned)((c1 - c0 + 127) / 128), (unsigned)(r1 - r0));
+    stencil2d_scalar_kernel<T, KIND><<<grid, 128, 0, s>>>(in, out, ld, r0, r1, c0, c1);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
+                           const int64_t* ub, cudaStream_t s) {
+  if (dtype == 0)
+    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lb, ub, s);
+  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lb, ub, s);
+}
+
+cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
+                            const int64_t* ub, cudaStream_t s) {
+  if (dtype == 0)
+    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lb, ub, s);
+  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lb, ub, s);
+}
+
+// =====================================================================================
+// 3-D 7-point stencil: a warp owns 32 column vectors of one (z, y) row and marches
+// in z keeping planes z-1, z, z+1 in registers; y neighbours are plain loads (their
+// rows are fetched by the neighbouring warps of the block, so they hit L1/L2).
+// =====================================================================================
+
+constexpr int S3_BY = 8;   // warps per block (rows in y)
+constexpr int S3_ZCH = 16; // planes per block
+
+template <typename T>
+__global__ void __launch_bounds__(32 * S3_BY) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                             int64_t n1, int64_t n2, int64_t z0, int64_t z1,
+                                                             int64_t y0, int64_t y1, int64_t x0, int64_t x1,
+                                                             int64_t xbase) {
+  constexpr int V = V16<T>::n;
+  const int lane = threadIdx.x;
+  const int64_t x = xbase + ((int64_t)blockIdx.x * 32 + lane) * V;
+  const int64_t y = y0 + (int64_t)blockIdx.y * S3_BY + threadIdx.y;
+  if (y >= y1) return;  // warp-uniform
+  const bool live = x < n2;
+  const int64_t zs = z0 + (int64_t)blockIdx.z * S3_ZCH;
+  const int64_t ze = min(zs + (int64_t)S3_ZCH, z1);
+  const int64_t plane = n1 * n2;
+  auto ld = [&](T(&r)[V], int64_t z, int64_t yy) {
+    if (live) {
+      V16<T>::load(r, in + z * plane + yy * n2 + x);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; v++) r[v] = T(0);
+    }
+  };
+  T zm[V], zc[V], zp[V], ym[V], yp[V];
+  ld(zm, zs - 1, y);
+  ld(zc, zs, y);
+  for (int64_t z = zs; z < ze; z++) {
+    ld(zp, z + 1, y);
+    ld(ym, z, y - 1);
+    ld(yp, z, y + 1);
+    T L = __shfl_up_sync(0xffffffffu, zc[V - 1], 1);
+    T R = __shfl_down_sync(0xffffffffu, zc[0], 1);
+    const T* row = in + z * plane + y * n2 + x;
+    if (lane == 0 && live) L = __ldg(row - 1);
+    if (lane == 31 && live) R = __ldg(row + V);
+    T o[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      const T xl = v == 0 ? L : zc[v - 1];
+      const T xr = v == V - 1 ? R : zc[v + 1];
+      T s = xl + xr;
+      s = s + ym[v];
+      s = s + yp[v];
+      s = s + zm[v];
+      s = s + zp[v];
+      o[v] = s / T(6);
+    }
+    if (live) {
+      T* dst = out + z * plane + y * n2 + x;
+      if (x >= x0 && x + V <= x1) {
+        V16<T>::store(dst, o);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; v++)
+          if (x + v >= x0 && x + v < x1) dst[v] = o[v];
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      zm[v] = zc[v];
+      zc[v] = zp[v];
+    }
+  }
+}
+
+template <typename T>
+__global__ void stencil7_scalar_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n1, int64_t n2,
+                                       int64_t z0, int64_t y0, int64_t y1, int64_t x0, int64_t x1) {
+  const int64_t x = x0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t y = y0 + blockIdx.y;
+  const int64_t z = z0 + blockIdx.z;
+  if (x >= x1 || y >= y1) return;
+  const int64_t pl = n1 * n2;
+  const T* p = in + z * pl + y * n2 + x;
+  T s = p[-1] + p[1];
+  s = s + p[-n2];
+  s = s + p[n2];
+  s = s + p[-pl];
+  s = s + p[pl];
+  out[z * pl + y * n2 + x] = s / T(6);
+}
+
+template <typename T>
+static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, const int64_t* lb,
+                                     const int64_t* ub, cudaStream_t s) {
+  const int64_t n1 = shape[1], n2 = shape[2];
+  if (lb[0] >= ub[0] || lb[1] >= ub[1] || lb[2] >= ub[2]) return cudaSuccess;
+  constexpr int V = V16<T>::n;
+  const bool vec = (n2 * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
+                   ((uintptr_t)out % 16) == 0;
+  if (vec) {
+    const int64_t xbase = lb[2] - (lb[2] % V);
+    const int64_t per = 32 * V;
+    dim3 grid((unsigned)((ub[2] - xbase + per - 1) / per), (unsigned)((ub[1] - lb[1] + S3_BY - 1) / S3_BY),
+              (unsigned)((ub[0] - lb[0] + S3_ZCH - 1) / S3_ZCH));
+    stencil7_kernel<T><<<grid, dim3(32, S3_BY), 0, s>>>(in, out, n1, n2, lb[0], ub[0], lb[1], ub[1], lb[2],
+                                                       ub[2], xbase);
+  } else {
+    dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));
+    stencil7_scalar_kernel<T><<<grid, 128, 0, s>>>(in, out, n1, n2, lb[0], lb[1], ub[1], lb[2], ub[2]);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
+                            const int64_t* ub, cudaStream_t s) {
+  if (dtype == 0) return launch_stencil7_t<double>((const double*)in, (double*)out, shape, lb, ub, s);
+  return launch_stencil7_t<float>((const float*)in, (float*)out, shape, lb, ub, s);
+}
+
+// =====================================================================================
+// elementwise: SCALE (X = alpha*X in X's arithmetic) and STAMP (splitmix64 raw bits)
+// =====================================================================================
+
+template <typename T>
+__device__ __forceinline__ T scale1(T x, double a);
+template <>
+__device__ __forceinline__ double scale1(double x, double a) { return a * x; }
+template <>
+__device__ __forceinline__ float scale1(float x, double a) { return (float)a * x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 scale1(__nv_bfloat16 x, double a) {
+  return __float2bfloat16_rn(__fmul_rn((float)a, __bfloat162float(x)));
+}
+
+// one block row per (i0, i1) run of the box; threads stride the contiguous dimension
+template <typename T>
+__global__ void __launch_bounds__(256) scale_kernel(T* x, int64_t n1, int64_t n2, int64_t lb0, int64_t lb1,
+                                                    int64_t lb2, int64_t e1, int64_t e2, int64_t runs, double a) {
+  for (int64_t run = blockIdx.y + (int64_t)blockIdx.z * gridDim.y; run < runs;
+       run += (int64_t)gridDim.y * gridDim.z) {
+    const int64_t i0 = run / e1, i1 = run - i0 * e1;
+    T* row = x + ((lb0 + i0) * n1 + (lb1 + i1)) * n2 + lb2;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < e2; j += (int64_t)gridDim.x * blockDim.x)
+      row[j] = scale1<T>(row[j], a);
+  }
+}
+
+cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb, const int64_t* ub,
+                         double alpha, cudaStream_t s) {
+  const int64_t e0 = ub[0] - lb[0], e1 = ub[1] - lb[1], e2 = ub[2] - lb[2];
+  if (e0 <= 0 || e1 <= 0 || e2 <= 0) return cudaSuccess;
+  const int64_t runs = e0 * e1;
+  unsigned gx = (unsigned)std::min<int64_t>((e2 + 255) / 256, 64);
+  int64_t gy = std::min<int64_t>(runs, 65535);
+  int64_t gz = std::min<int64_t>((runs + gy - 1) / gy, 64);
+  dim3 grid(gx, (unsigned)gy, (unsigned)gz);
+  if (dtype == 0)
+    scale_kernel<double><<<grid, 256, 0, s>>>((double*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha);
+  else if (dtype == 1)
+    scale_kernel<float><<<grid, 256, 0, s>>>((float*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha);
+  else
+    scale_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1,
+                                                      e2, runs, alpha);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  unsigned long long z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void stamp_kernel(char* x, int es, int64_t n1, int64_t n2, const __grid_constant__ BoxList bl,
+                             unsigned long long seed) {
+  const unsigned long long base = seed * 0x9E3779B97F4A7C15ULL;
+  for (int b = 0; b < bl.n; b++) {
+    const int64_t e0 = bl.ub[b][0] - bl.lb[b][0], e1 = bl.ub[b][1] - bl.lb[b][1], e2 = bl.ub[b][2] - bl.lb[b][2];
+    const int64_t n = e0 * e1 * e2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i0 = t / (e1 * e2), r = t - i0 * e1 * e2, i1 = r / e2, i2 = r - i1 * e2;
+      const int64_t c = ((bl.lb[b][0] + i0) * n1 + (bl.lb[b][1] + i1)) * n2 + (bl.lb[b][2] + i2);
+      const unsigned long long h = splitmix64(base + (unsigned long long)c);
+      char* p = x + c * es;
+      if (es == 8) *reinterpret_cast<unsigned long long*>(p) = h;
+      else if (es == 4) *reinterpret_cast<unsigned int*>(p) = (unsigned int)h;
+      else *reinterpret_cast<unsigned short*>(p) = (unsigned short)h;
+    }
+  }
+}
+
+cudaError_t launch_stamp(int es, void* x, const int64_t* shape, const BoxList& boxes, unsigned long long seed,
+                         cudaStream_t s) {
+  if (boxes.n <= 0) return cudaSuccess;
+  stamp_kernel<<<148 * 4, 256, 0, s>>>((char*)x, es, shape[1], shape[2], boxes, seed);
+  return cudaGetLastError();
+}
+
+}  // namespace hda

@@ -1,0 +1,79 @@
+// kernels.cuh — launch interfaces of the sm_100a kernels (library-internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hda {
+
+// One strided rectangle copy, raw bytes: n0 x n1 runs of run_bytes contiguous bytes.
+// Run (i0, i1) starts at src + src_off + i0*src_p0 + i1*src_p1 (same for dst).
+// Used for the fused pull (peer replica -> local replica, same offsets on both sides:
+// pack + NVLink transfer + unpack in one pass), for pack (replica -> contiguous
+// staging), unpack (staging -> replica) and the COPY kernel (replica -> replica).
+struct RunDesc {
+  const char* src;
+  char* dst;
+  int64_t src_off, dst_off;
+  int64_t src_p0, dst_p0;
+  int64_t src_p1, dst_p1;
+  int64_t run_bytes;
+  int64_t unit_begin;   // first work unit of this descriptor (prefix sum)
+  int32_t n0, n1;
+  int32_t es;           // element size: granularity of heads/tails/misaligned copies
+  int32_t chunks;       // >0: long runs, chunks per run (one warp per chunk)
+                        // 0 : short runs, 32 runs per unit (one thread per run)
+};
+
+constexpr int kMaxRunDescs = 24;
+struct RunBatch {
+  RunDesc d[kMaxRunDescs];
+  int32_t n;
+  int64_t total_units;
+};
+constexpr int64_t kChunkBytes = 8192;
+
+// sets chunks/unit_begin and returns the number of units of one descriptor
+int64_t run_desc_units(RunDesc& d);
+
+// cross-device ordering words (see hda.cpp "sync protocol")
+constexpr int kMaxDev = 64;
+struct WaitList {
+  unsigned long long* ptr[kMaxDev];
+  unsigned long long val[kMaxDev];
+  int32_t n;
+};
+struct SignalList {
+  unsigned long long* ptr[kMaxDev];
+  int32_t n;
+  unsigned long long val;
+};
+
+struct BoxList {  // boxes in element coordinates of a 3-D padded shape
+  int64_t lb[16][3];
+  int64_t ub[16][3];
+  int32_t n;
+};
+
+cudaError_t launch_copy_runs(const RunBatch& b, cudaStream_t s);
+cudaError_t launch_wait(const WaitList& w, int* err_flag, long long timeout_ns, cudaStream_t s);
+cudaError_t launch_signal(const SignalList& l, cudaStream_t s);
+
+// user kernels over the work box [lb, ub) of one device's replica (padded 3-D shape)
+cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
+                           const int64_t* lb, const int64_t* ub, cudaStream_t s);
+cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape,
+                            const int64_t* lb, const int64_t* ub, cudaStream_t s);
+cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape,
+                            const int64_t* lb, const int64_t* ub, cudaStream_t s);
+cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb,
+                         const int64_t* ub, double alpha, cudaStream_t s);
+cudaError_t launch_stamp(int es, void* x, const int64_t* shape, const BoxList& boxes,
+                         unsigned long long seed, cudaStream_t s);
+// C[rows lb0..ub0, cols lb1..ub1] = alpha * A@B + beta*C ; A [M,K] bf16 row-major,
+// B [K,N] bf16 row-major, C [M,N] f32 or bf16 row-major (full-array strides)
+cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N,
+                        int64_t K, const int64_t* lb, const int64_t* ub, float alpha, float beta,
+                        cudaStream_t s);
+
+}  // namespace hda

@@ -1,0 +1,337 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by
+element on the same seeded inputs.
+
+Bars (BASELINE.json north_star): message sets, owner maps and exchanged data
+bit-exact; stencils within 1e-12 normwise (they are in fact compared bit-exactly:
+both sides use the same operand order and IEEE operations); the product within
+1e-2 relative Frobenius (integer cases bit-exact).  Every replica of every device is
+compared, so out-of-region writes and stale halos are caught.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from programs import LibAdapter, gen_program, run_program
+
+pytestmark = pytest.mark.gpu
+
+J = [(0, -1), (0, 1), (-1, 0), (1, 0)]
+N9 = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1) if i or j]
+N7 = [(0, 0, -1), (0, 0, 1), (0, -1, 0), (0, 1, 0), (-1, 0, 0), (1, 0, 0)]
+
+
+@pytest.fixture(scope="module")
+def H():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    import paper_1809_05657_b200 as H
+    H.lib()
+    return H
+
+
+def ngpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+def assert_same_msgs(h, w):
+    a = O.msgs_by_pair(LibAdapter(h).msgs())
+    b = O.msgs_by_pair(w.msgs())
+    assert a.keys() == b.keys()
+    for k in b:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def assert_replicas(h, w, arrs, P):
+    for a in arrs:
+        np.testing.assert_array_equal(h.owner_map(a), w.owner_map(a))
+        for d in range(P):
+            g = h.read_replica(a, d)
+            o = w.replica(a, d)
+            assert g.tobytes() == o.tobytes(), f"array {a} device {d}: replica differs"
+
+
+# ------------------------------------------------------------------ config 1
+@pytest.mark.parametrize("transport", [0, 1])
+def test_config1_virtual_devices(H, transport):
+    """BASELINE configs[0]: 16x16 fp64 Jacobi, 4 row partitions, +-1 offsets; paper
+    2-call form on one GPU with 4 virtual devices."""
+    n, P = 16, 4
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    h.set_transport(transport)
+    w = O.Oracle(P)
+    init_a = synth.uniform(synth.SEED0 + 0, (n, n))
+    init_b = synth.uniform(synth.SEED0 + 100, (n, n))
+    for be in (h, w):
+        A = be.create(H.F64, (n, n))
+        B = be.create(H.F64, (n, n))
+        data = be.partition(H.ROW, (n, n))
+        work = be.partition(H.ROW, (n, n), (1, 1), (n - 1, n - 1))
+        be.write(A, data, init_a)
+        be.write(B, data, init_b)
+    assert_replicas(h, w, [A, B], P)
+    for s in range(3):
+        for be in (h, w):
+            be.apply(H.K_JACOBI5, work, [(A, [], [(0, 0)]), (B, J, [])])
+        assert_same_msgs(h, w)
+        assert_replicas(h, w, [A, B], P)
+        for be in (h, w):
+            be.apply(H.K_COPY, work, [(B, [], [(0, 0)]), (A, [(0, 0)], [])])
+        assert_same_msgs(h, w)
+        assert_replicas(h, w, [A, B], P)
+    got = h.read(B, data)
+    ref = w.read(B, data)
+    assert_same_msgs(h, w)
+    assert got.tobytes() == ref.tobytes()
+    assert h.stats()["plan_hits"] > 0
+    h.close()
+
+
+# ------------------------------------------------------------------ random programs
+@pytest.mark.parametrize("P,transport", [(2, 0), (3, 1), (4, 0), (8, 0), (8, 1)])
+def test_random_programs_bit_exact(H, P, transport):
+    """STAMP writes distinctive raw bits (NaN payloads included) on arbitrary def
+    shapes; reads/writes/partition switches move them; every replica must match."""
+    for seed in range(12):
+        for ndim in (2, 3):
+            prog = gen_program(50_000 + 100 * P + seed, P, ndim=ndim, n_ops=8, with_kernels=True)
+            w = O.Oracle(P)
+            h = H.HDArray(n_gpus=1, n_devices=P)
+            h.set_transport(transport)
+            lib = LibAdapter(h)
+            states = {}
+
+            def on_o(step, op, arrs, st):
+                states[step] = (st, O.msgs_by_pair(w.msgs()) if st == 0 else None,
+                                [[w.replica(a, d).tobytes() for d in range(P)] for a in arrs])
+
+            def on_l(step, op, arrs, st):
+                st_o, m_o, reps = states[step]
+                assert st == st_o
+                if st == 0:
+                    m_l = O.msgs_by_pair(lib.msgs())
+                    assert m_l.keys() == m_o.keys()
+                for ai, a in enumerate(arrs):
+                    for d in range(P):
+                        assert h.read_replica(a, d).tobytes() == reps[ai][d], (seed, step, op, a, d)
+
+            run_program(prog, w, on_o)
+            run_program(prog, lib, on_l)
+            h.close()
+
+
+# ------------------------------------------------------------------ stencils
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("shape,kind,P", [((150, 700), "ROW", 3), ((130, 1030), "BLOCK", 4),
+                                          ((37, 53), "COL", 2), ((300, 260), "BLOCK", 8)])
+def test_stencil2d_bit_exact(H, dtype, shape, kind, P):
+    DT = H.F64 if dtype == "f64" else H.F32
+    npdt = np.float64 if dtype == "f64" else np.float32
+    u0 = synth.uniform(synth.SEED0 + 1, shape, dtype)
+    for K, uses in ((H.K_JACOBI5, J), (H.K_STENCIL9, N9)):
+        h = H.HDArray(n_gpus=1, n_devices=P)
+        w = O.Oracle(P)
+        for be in (h, w):
+            X = be.create(DT, shape, u0)
+            Y = be.create(DT, shape, u0)
+            part = be.partition(getattr(H, kind), shape, (1, 1), (shape[0] - 1, shape[1] - 1))
+            for s in range(4):
+                src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+                be.apply(K, part, [(dst, [], [(0, 0)]), (src, uses, [])])
+        assert_replicas(h, w, [X, Y], P)
+        assert h.read_replica(X, 0).dtype == npdt
+        h.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_stencil7_3d_bit_exact(H, dtype):
+    DT = H.F64 if dtype == "f64" else H.F32
+    shape, P = (40, 36, 70), 3
+    u0 = synth.uniform(synth.SEED0 + 4, shape, dtype)
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    for be in (h, w):
+        X = be.create(DT, shape, u0)
+        Y = be.create(DT, shape, u0)
+        part = be.partition(H.ROW, shape, (1, 1, 1), tuple(s - 1 for s in shape))
+        for s in range(3):
+            src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+            be.apply(H.K_STENCIL7_3D, part, [(dst, [], [(0, 0, 0)]), (src, N7, [])])
+    assert_replicas(h, w, [X, Y], P)
+    h.close()
+
+
+# ------------------------------------------------------------------ repartition
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
+@pytest.mark.parametrize("transport", [0, 1])
+def test_repartition_row_col(H, dtype, transport):
+    """configs[3] at test scale: ROW SCALE then COL SCALE on X; each switch is a full
+    P(P-1)-block redistribution."""
+    DT = {"f32": H.F32, "bf16": H.BF16, "f64": H.F64}[dtype]
+    shape, P = (96, 160), 4
+    v = synth.uniform(9, shape, dtype)
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    h.set_transport(transport)
+    w = O.Oracle(P)
+    for be in (h, w):
+        X = be.create(DT, shape)
+        rowp = be.partition(H.ROW, shape)
+        colp = be.partition(H.COL, shape)
+        be.write(X, rowp, v)
+    for it in range(3):
+        for part in (colp, rowp):
+            for be in (h, w):
+                be.apply(H.K_SCALE, part, [(X, [(0, 0)], [(0, 0)])], [1.5 if it % 2 else 0.5])
+            assert_same_msgs(h, w)
+            n_blocks = len(O.msgs_by_pair(w.msgs()))
+            assert n_blocks == P * (P - 1)
+            assert_replicas(h, w, [X], P)
+    h.close()
+
+
+def test_raw_bits_repartition(H):
+    """random bit patterns (NaN payloads, denormals, infinities) survive the exchange
+    bit-exactly: write under ROW, read under COL (pure copies)."""
+    shape, P = (64, 96), 4
+    for dt, name in ((H.F64, "f64"), (H.F32, "f32"), (H.BF16, "bf16")):
+        bits = synth.random_bits(77, shape, name)
+        for transport in (0, 1):
+            h = H.HDArray(n_gpus=1, n_devices=P)
+            h.set_transport(transport)
+            X = h.create(dt, shape)
+            h.write(X, h.partition(H.ROW, shape), bits)
+            got = h.read(X, h.partition(H.COL, shape))
+            assert got.tobytes() == np.ascontiguousarray(bits).tobytes()
+            assert h.stats()["last_msgs"] == P * (P - 1)
+            h.close()
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("cdt", ["f32", "bf16"])
+def test_gemm_integer_exact_and_allgather(H, cdt):
+    """Listing 2 with integer bf16 inputs: fp32 accumulation is exact
+    (|sum| < 2^24), so C is bit-exact vs int64 matmul; call 1 all-gathers B."""
+    M, N, K, P = 256, 384, 512, 2
+    Ab = synth.int_bf16(21, (M, K))
+    Bb = synth.int_bf16(22, (K, N))
+    exact = synth.bf16_to_f32(Ab).astype(np.int64) @ synth.bf16_to_f32(Bb).astype(np.int64)
+    CT = H.F32 if cdt == "f32" else H.BF16
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    S = H.STAR
+    for be in (h, w):
+        A = be.create(H.BF16, (M, K))
+        B = be.create(H.BF16, (K, N))
+        C = be.create(CT, (M, N))
+        pa, pb, pc = be.partition(H.ROW, (M, K)), be.partition(H.ROW, (K, N)), be.partition(H.ROW, (M, N))
+        be.write(A, pa, Ab)
+        be.write(B, pb, Bb)
+        be.apply(H.K_GEMM, pc, [(C, [], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.0, 0.0])
+    assert_same_msgs(h, w)
+    assert len(O.msgs_by_pair(w.msgs())) == P * (P - 1)
+    got = h.read(C, pc)
+    ref = w.read(C, pc)
+    assert got.tobytes() == ref.tobytes()
+    if cdt == "f32":
+        np.testing.assert_array_equal(got.astype(np.int64), exact)
+    for be in (h, w):
+        be.apply(H.K_GEMM, pc, [(C, [], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.0, 0.0])
+    assert h.stats()["last_msgs"] == 0 and len(w.msgs()) == 0
+    h.close()
+
+
+def test_gemm_random_frobenius(H):
+    M, N, K, P = 320, 256, 448, 4
+    Ab = synth.uniform(31, (M, K), "bf16")
+    Bb = synth.uniform(32, (K, N), "bf16")
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    S = H.STAR
+    Cin = synth.uniform(33, (M, N), "f32")
+    for be in (h, w):
+        A = be.create(H.BF16, (M, K), Ab)
+        B = be.create(H.BF16, (K, N), Bb)
+        C = be.create(H.F32, (M, N), Cin)
+        pc = be.partition(H.BLOCK, (M, N))
+        be.apply(H.K_GEMM, pc, [(C, [(0, 0)], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.25, -0.5])
+    got = h.read(C, pc).astype(np.float64)
+    ref = w.read(C, pc).astype(np.float64)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-2
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-5  # fp32 accumulation
+    h.close()
+
+
+# ------------------------------------------------------------------ full scale
+def test_config2_full_scale_eigenmode(H):
+    """configs[1] at full size on one GPU: 8192^2 fp64 Jacobi, ROW, ping-pong, 100
+    sweeps, in the bench launch configuration.  Closed form u = lambda^s u0
+    within 1e-12 normwise, plus sampled cells against the oracle on windows."""
+    n, sweeps, a, b = 8192, 100, 37, 61
+    u0 = synth.eigenmode2d(n, n, a, b)
+    lam = (np.cos(a * np.pi / (n - 1)) + np.cos(b * np.pi / (n - 1))) / 2
+    h = H.HDArray(n_gpus=1, n_devices=1)
+    X = h.create(H.F64, (n, n), u0)
+    Y = h.create(H.F64, (n, n), u0)
+    part = h.partition(H.ROW, (n, n), (1, 1), (n - 1, n - 1))
+    for s in range(sweeps):
+        src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+        h.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+    got = h.read(X, h.partition(H.ROW, (n, n)))
+    ref = lam ** sweeps * u0
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) < 1e-12
+    # sampled cells: the oracle on a (2s+3)^2 window around each sample, from the
+    # random initial field (a window of radius s+1 makes the centre exact)
+    s = 6
+    v0 = synth.uniform(synth.SEED0 + 1, (n, n))
+    h2 = H.HDArray(n_gpus=1, n_devices=1)
+    X = h2.create(H.F64, (n, n), v0)
+    Y = h2.create(H.F64, (n, n), v0)
+    for k in range(s):
+        src, dst = (X, Y) if k % 2 == 0 else (Y, X)
+        h2.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+    full = h2.read(X, h2.partition(H.ROW, (n, n)))
+    rng = np.random.default_rng(5)
+    pts = [(1, 1), (n - 2, n - 2), (1, n - 2), (4000, 17)] + [tuple(rng.integers(1, n - 1, 2)) for _ in range(6)]
+    r = s + 1
+    for (i, j) in pts:
+        i0, i1 = max(i - r, 0), min(i + r + 1, n)
+        j0, j1 = max(j - r, 0), min(j + r + 1, n)
+        win = np.ascontiguousarray(v0[i0:i1, j0:j1])
+        w = O.Oracle(1)
+        WX = w.create(O.F64, win.shape, win)
+        WY = w.create(O.F64, win.shape, win)
+        # interior of the window; array borders keep their ghost role
+        lb = (1 if i0 == 0 else 1, 1 if j0 == 0 else 1)
+        wp = w.partition(O.ROW, win.shape, lb, (win.shape[0] - 1, win.shape[1] - 1))
+        for k in range(s):
+            src, dst = (WX, WY) if k % 2 == 0 else (WY, WX)
+            w.apply(O.K_JACOBI5, wp, [(dst, [], [(0, 0)]), (src, J, [])])
+        ow = w.replica(WX, 0)
+        assert ow[i - i0, j - j0] == full[i, j], (i, j)
+    h.close()
+    h2.close()
+
+
+# ------------------------------------------------------------------ multi-GPU
+@pytest.mark.skipif("ngpus() < 2")
+@pytest.mark.parametrize("P", [2, 4])
+def test_multi_gpu_single_process(H, P):
+    """P devices over 2 physical GPUs (NVLink peer pulls + cross-GPU sync words)."""
+    shape = (258, 514)
+    u0 = synth.uniform(3, shape)
+    for transport in (0, 1):
+        h = H.HDArray(n_gpus=2, n_devices=P)
+        h.set_transport(transport)
+        w = O.Oracle(P)
+        for be in (h, w):
+            X = be.create(H.F64, shape, u0)
+            Y = be.create(H.F64, shape, u0)
+            part = be.partition(H.ROW, shape, (1, 1), (shape[0] - 1, shape[1] - 1))
+            colp = be.partition(H.COL, shape)
+            for s in range(6):
+                src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+                be.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+            be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
+        assert_replicas(h, w, [X, Y], P)
+        h.close()
