@@ -83,9 +83,4 @@ cudaError_t launch_gemm_simt(int c_dtype, const void* A, const void* B, void* C,
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
-                        const int64_t* lb, const int64_t* ub, float alpha, float beta, cudaStream_t s) {
-  return launch_gemm_simt(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, s);
-}
-
 }  // namespace hda

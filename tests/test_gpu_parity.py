@@ -287,9 +287,10 @@ def test_config2_full_scale_eigenmode(H):
     h2 = H.HDArray(n_gpus=1, n_devices=1)
     X = h2.create(H.F64, (n, n), v0)
     Y = h2.create(H.F64, (n, n), v0)
+    part2 = h2.partition(H.ROW, (n, n), (1, 1), (n - 1, n - 1))
     for k in range(s):
         src, dst = (X, Y) if k % 2 == 0 else (Y, X)
-        h2.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+        h2.apply(H.K_JACOBI5, part2, [(dst, [], [(0, 0)]), (src, J, [])])
     full = h2.read(X, h2.partition(H.ROW, (n, n)))
     rng = np.random.default_rng(5)
     pts = [(1, 1), (n - 2, n - 2), (1, n - 2), (4000, 17)] + [tuple(rng.integers(1, n - 1, 2)) for _ in range(6)]
