@@ -304,7 +304,8 @@ def main():
     # ---- parity against the closed form (eigenmode) on this rank's rows
     lam = (np.cos(a_mode * np.pi / (n - 1)) + np.cos(b_mode * np.pi / (n - 1))) / 2
     got = h.read(state["src"], data)
-    rows = slice(my_lb[0], my_ub[0])
+    d_lb, d_ub = h.region(data, rank, 2)
+    rows = slice(max(my_lb[0], d_lb[0]), min(my_ub[0], d_ub[0]))
     ref = lam ** sweeps_done[0] * u0[rows]
     err = float(np.max(np.abs(got[rows] - ref)) / np.max(np.abs(ref)))
     err = max_over_ranks(err)

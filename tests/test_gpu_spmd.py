@@ -1,0 +1,96 @@
+"""SPMD mode on >= 2 GPUs: one process per GPU (the bench's torchrun layout), peer
+replicas mapped with CUDA IPC, device-side sync words.  Each rank compares its own
+replica with the oracle after every call (bit-exact), for halo exchange (ROW Jacobi,
+BLOCK 9-point with corners) and a ROW<->COL repartition."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+J = [(0, -1), (0, 1), (-1, 0), (1, 0)]
+N9 = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1) if i or j]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle as O
+        import paper_1809_05657_b200 as H
+        import synth
+        h = H.HDArray.spmd(world, rank, rank)
+        w = O.Oracle(world)
+        shape = (130, 262)
+        u0 = synth.uniform(5, shape)
+        bad = []
+
+        def check(tag, arrs):
+            for a in arrs:
+                if h.read_replica(a, rank).tobytes() != w.replica(a, rank).tobytes():
+                    bad.append((tag, a))
+                if not (h.owner_map(a) == w.owner_map(a)).all():
+                    bad.append((tag, "owner", a))
+
+        for be in (h, w):
+            X = be.create(H.F64, shape, u0)
+            Y = be.create(H.F64, shape, u0)
+            rowp = be.partition(H.ROW, shape, (1, 1), (shape[0] - 1, shape[1] - 1))
+            blk = be.partition(H.BLOCK, shape, (1, 1), (shape[0] - 1, shape[1] - 1))
+            colp = be.partition(H.COL, shape)
+            full = be.partition(H.ROW, shape)
+        for it in range(4):
+            for be in (h, w):
+                be.apply(H.K_JACOBI5, rowp, [(Y, [], [(0, 0)]), (X, J, [])])
+                be.apply(H.K_STENCIL9, blk, [(X, [], [(0, 0)]), (Y, N9, [])])
+            check(f"it{it}", [X, Y])
+        for be in (h, w):
+            be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
+            be.apply(H.K_SCALE, full, [(X, [(0, 0)], [(0, 0)])], [0.5])
+        check("repart", [X])
+        got = h.read(X, full)
+        ref = w.read(X, full)
+        lb, ub = h.region(full, rank, 2)
+        if got[lb[0]:ub[0]].tobytes() != ref[lb[0]:ub[0]].tobytes():
+            bad.append(("read",))
+        st = h.stats()
+        h.close()
+        dist.destroy_process_group()
+        q.put((rank, bad, st["msgs_total"], st["plan_hits"]))
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+        q.put((rank, ["exception", traceback.format_exc()], 0, 0))
+
+
+def test_spmd_two_gpus():
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=240) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, bad, msgs, hits in out:
+        assert not bad, (rank, bad)
+        assert msgs > 0 and hits > 0

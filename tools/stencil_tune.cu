@@ -1,0 +1,283 @@
+// stencil_tune.cu — standalone timing of fp64 Jacobi kernel designs on 8192^2
+// (configs[1]); not part of the library.  Build: nvcc -gencode arch=compute_100a,code=sm_100a
+// -O3 -std=c++17 tools/stencil_tune.cu -o stencil_tune -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e = (x);                                                           \
+    if (e != cudaSuccess) {                                                        \
+      printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__);     \
+      exit(1);                                                                     \
+    }                                                                              \
+  } while (0)
+
+// ------------------------------------------------------------- A/B/D: register march
+template <int ROWS, int GROUP, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) march(const double* __restrict__ in, double* __restrict__ out,
+                                                       long ld, long r0, long r1, long c0, long c1, long cbase) {
+  constexpr int V = 2;
+  constexpr int W = GROUP + 2;
+  const int lane = threadIdx.x & 31;
+  const long col = cbase + ((long)blockIdx.x * THREADS + threadIdx.x) * V;
+  const bool live = col < ld;
+  const long rs = r0 + (long)blockIdx.y * ROWS;
+  const long re = min(rs + (long)ROWS, r1);
+  double w[W][V];
+  auto ldr = [&](double(&r)[V], long row) {
+    if (live) {
+      double2 v = __ldg(reinterpret_cast<const double2*>(in + row * ld + col));
+      r[0] = v.x;
+      r[1] = v.y;
+    } else {
+      r[0] = r[1] = 0;
+    }
+  };
+  ldr(w[0], rs - 1);
+  ldr(w[1], rs);
+  for (long base = rs; base < re; base += GROUP) {
+#pragma unroll
+    for (int k = 0; k < GROUP; k++)
+      if (base + 1 + k <= re) ldr(w[k + 2], base + 1 + k);
+#pragma unroll
+    for (int k = 0; k < GROUP; k++) {
+      const long r = base + k;
+      if (r >= re) break;
+      double L = __shfl_up_sync(0xffffffffu, w[k + 1][1], 1);
+      double R = __shfl_down_sync(0xffffffffu, w[k + 1][0], 1);
+      if (lane == 0 && live) L = __ldg(in + r * ld + col - 1);
+      if (lane == 31 && live) R = __ldg(in + r * ld + col + 2);
+      double o0 = (((L + w[k + 1][1]) + w[k][0]) + w[k + 2][0]) * 0.25;
+      double o1 = (((w[k + 1][0] + R) + w[k][1]) + w[k + 2][1]) * 0.25;
+      if (live) {
+        double* d = out + r * ld + col;
+        if (col >= c0 && col + 2 <= c1)
+          *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+        else {
+          if (col >= c0 && col < c1) d[0] = o0;
+          if (col + 1 >= c0 && col + 1 < c1) d[1] = o1;
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+      w[0][v] = w[GROUP][v];
+      w[1][v] = w[GROUP + 1][v];
+    }
+  }
+}
+
+// ------------------------------------------------------------- C: one vector per thread
+__global__ void __launch_bounds__(256) simple(const double* __restrict__ in, double* __restrict__ out, long ld,
+                                              long r0, long r1, long c0, long c1, long cbase) {
+  const int lane = threadIdx.x & 31;
+  const long col = cbase + ((long)blockIdx.x * 64 + threadIdx.x % 64) * 2;
+  const long r = r0 + (long)blockIdx.y * 4 + threadIdx.x / 64;
+  if (r >= r1) return;
+  const bool live = col < ld;
+  double2 up = make_double2(0, 0), cu = up, dn = up;
+  if (live) {
+    up = __ldg(reinterpret_cast<const double2*>(in + (r - 1) * ld + col));
+    cu = __ldg(reinterpret_cast<const double2*>(in + r * ld + col));
+    dn = __ldg(reinterpret_cast<const double2*>(in + (r + 1) * ld + col));
+  }
+  double L = __shfl_up_sync(0xffffffffu, cu.y, 1);
+  double R = __shfl_down_sync(0xffffffffu, cu.x, 1);
+  if (lane == 0 && live) L = __ldg(in + r * ld + col - 1);
+  if (lane == 31 && live) R = __ldg(in + r * ld + col + 2);
+  double o0 = (((L + cu.y) + up.x) + dn.x) * 0.25;
+  double o1 = (((cu.x + R) + up.y) + dn.y) * 0.25;
+  if (live) {
+    double* d = out + r * ld + col;
+    if (col >= c0 && col + 2 <= c1)
+      *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+    else {
+      if (col >= c0 && col < c1) d[0] = o0;
+      if (col + 1 >= c0 && col + 1 < c1) d[1] = o1;
+    }
+  }
+}
+
+// ------------------------------------------------------------- E: TMA tiles in smem
+namespace e {
+constexpr int BOXW = 256, OUTW = 248, TH = 30, BOXH = TH + 2, STAGES = 3, THREADS = 256;
+constexpr int STAGE_BYTES = BOXW * BOXH * 8;
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
+          sa(b)),
+      "r"(ph)
+      : "memory");
+}
+__global__ void __launch_bounds__(THREADS, 1) tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                         double* __restrict__ out, long ld, long r0, long r1, long c0,
+                                                         long c1, long n_ct, long n_rt) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  double* tiles = reinterpret_cast<double*>(sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + STAGES * STAGE_BYTES);
+  const int t = threadIdx.x;
+  const long total = n_ct * n_rt;
+  const long per = (total + gridDim.x - 1) / gridDim.x;
+  const long t0 = blockIdx.x * per, t1 = min(total, t0 + per);
+  if (t == 0) {
+    for (int s = 0; s < STAGES; s++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&full[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](long tile, int s) {
+    const long ct = tile / n_rt, rt = tile % n_rt;
+    const int x = (int)(c0 + ct * OUTW - 4), y = (int)(r0 + rt * TH - 1);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(STAGE_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            sa(tiles + (size_t)s * BOXW * BOXH)),
+        "l"(&map), "r"(sa(&full[s])), "r"(x), "r"(y)
+        : "memory");
+  };
+  if (t == 0)
+    for (int s = 0; s < STAGES - 1 && t0 + s < t1; s++) issue(t0 + s, s);
+  int s = 0;
+  uint32_t ph = 0;
+  for (long tile = t0; tile < t1; tile++) {
+    if (t == 0 && tile + STAGES - 1 < t1) issue(tile + STAGES - 1, (s + STAGES - 1) % STAGES);
+    wait(&full[s], ph);
+    const long ct = tile / n_rt, rt = tile % n_rt;
+    const double* S = tiles + (size_t)s * BOXW * BOXH;
+    if (t < OUTW) {
+      const long col = c0 + ct * OUTW + t;
+      const int x = t + 4;
+      double up = S[x], cu = S[BOXW + x];
+#pragma unroll 6
+      for (int rr = 0; rr < TH; rr++) {
+        const double* row = S + (rr + 1) * BOXW;
+        double dn = row[BOXW + x];
+        double o = (((row[x - 1] + row[x + 1]) + up) + dn) * 0.25;
+        const long r = r0 + rt * TH + rr;
+        if (r < r1 && col < c1) out[r * ld + col] = o;
+        up = cu;
+        cu = dn;
+      }
+    }
+    __syncthreads();  // stage s fully consumed before it is refilled
+    if (++s == STAGES) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+}
+}  // namespace e
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+  const long n = 8192;
+  const size_t bytes = n * n * 8;
+  double *X, *Y, *R;
+  CK(cudaMalloc(&X, bytes));
+  CK(cudaMalloc(&Y, bytes));
+  CK(cudaMalloc(&R, bytes));
+  std::vector<double> h(n * n);
+  for (long i = 0; i < n * n; i++) h[i] = (double)((i * 2654435761u) % 1000) / 1000.0;
+  CK(cudaMemcpy(X, h.data(), bytes, cudaMemcpyHostToDevice));
+  const long r0 = 1, r1 = n - 1, c0 = 1, c1 = n - 1;
+  const double alg = (double)(r1 - r0) * (c1 - c0) * 16;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto time_it = [&](const char* name, auto launch) {
+    CK(cudaMemset(Y, 0, bytes));
+    for (int i = 0; i < 5; i++) launch();
+    CK(cudaDeviceSynchronize());
+    const int it = 200;
+    cudaEventRecord(a);
+    for (int i = 0; i < it; i++) launch();
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    double us = ms * 1e3 / it;
+    // correctness vs reference (variant A output in R)
+    std::vector<double> o(n * n), ref(n * n);
+    CK(cudaMemcpy(o.data(), Y, bytes, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ref.data(), R, bytes, cudaMemcpyDeviceToHost));
+    long bad = 0;
+    for (long i = 0; i < n * n; i++) bad += o[i] != ref[i];
+    printf("%-28s %8.1f us  %7.1f GB/s  mismatches=%ld\n", name, us, alg / us / 1e3, bad);
+  };
+  const long cbase = 0;
+  // reference output
+  {
+    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
+    march<32, 8, 128, 1><<<g, 128>>>(X, R, n, r0, r1, c0, c1, cbase);
+    CK(cudaDeviceSynchronize());
+  }
+  time_it("A march R32 G8 T128", [&] {
+    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
+    march<32, 8, 128, 1><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  time_it("B march R32 G4 T128 minB8", [&] {
+    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
+    march<32, 4, 128, 8><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  time_it("B2 march R64 G4 T128 minB8", [&] {
+    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 63) / 64));
+    march<64, 4, 128, 8><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  time_it("B3 march R16 G4 T256 minB4", [&] {
+    dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + 15) / 16));
+    march<16, 4, 256, 4><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  time_it("D march R32 G8 T128 minB6", [&] {
+    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
+    march<32, 8, 128, 6><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  time_it("D2 march R128 G8 T128 minB6", [&] {
+    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 127) / 128));
+    march<128, 8, 128, 6><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  time_it("C simple", [&] {
+    dim3 g((unsigned)((c1 - cbase + 127) / 128), (unsigned)((r1 - r0 + 3) / 4));
+    simple<<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);
+  });
+  // E: TMA
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+  cuuint64_t str[1] = {(cuuint64_t)n * 8};
+  cuuint32_t box[2] = {e::BOXW, e::BOXH};
+  cuuint32_t es[2] = {1, 1};
+  CUresult cr = ((EncodeFn)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, X, dims, str, box, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) printf("encode failed %d\n", (int)cr);
+  const int smem = e::STAGES * e::STAGE_BYTES + 64;
+  CK(cudaFuncSetAttribute(e::tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const long n_ct = (c1 - c0 + e::OUTW - 1) / e::OUTW, n_rt = (r1 - r0 + e::TH - 1) / e::TH;
+  for (int grid : {148, 296}) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "E tma grid%d", grid);
+    time_it(nm, [&] { e::tma_kernel<<<grid, e::THREADS, smem>>>(map, Y, n, r0, r1, c0, c1, n_ct, n_rt); });
+  }
+  // plain copy for reference bandwidth
+  {
+    cudaEventRecord(a);
+    for (int i = 0; i < 50; i++) cudaMemcpyAsync(Y, X, bytes, cudaMemcpyDeviceToDevice);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("%-28s %8.1f us  %7.1f GB/s\n", "cudaMemcpy D2D", ms * 1e3 / 50, 2.0 * bytes / (ms * 1e-3 / 50) / 1e9);
+  }
+  return 0;
+}
