@@ -26,6 +26,8 @@ import time
 
 import numpy as np
 
+import synth
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -162,19 +164,218 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- workloads
+N9 = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1) if i or j]
+N7 = [(0, 0, -1), (0, 0, 1), (0, -1, 0), (0, 1, 0), (-1, 0, 0), (1, 0, 0)]
+
+
+class Stencil:
+    """configs[1] (jacobi2d), configs[2] (stencil9) and the 3-D half of configs[4]
+    (stencil7): ping-pong sweeps over the interior, eigenmode inputs (closed-form parity)."""
+
+    def __init__(self, kind, H, h, rank, ws, n=None):
+        self.kind, self.H, self.h, self.rank, self.ws = kind, H, h, rank, ws
+        if kind == "jacobi2d":
+            self.n = n or 8192
+            self.shape, self.dt, self.es = (self.n, self.n), H.F64, 8
+            self.K, self.uses, self.part_kind = H.K_JACOBI5, J, H.ROW
+            self.modes = (37, 61)
+            self.workload = (f"configs[1]: {self.n}x{self.n} fp64 Jacobi (P:L459), ROW partition of the interior, "
+                             "ping-pong sweeps through hda_apply")
+            self.kname = "stencil2d_kernel<double,JACOBI5>"
+        elif kind == "stencil9":
+            self.n = n or 16384
+            self.shape, self.dt, self.es = (self.n, self.n), H.F64, 8
+            self.K, self.uses, self.part_kind = H.K_STENCIL9, N9, H.BLOCK
+            self.modes = (3, 4)
+            self.workload = (f"configs[2]: {self.n}x{self.n} fp64 9-point stencil (R12), BLOCK partition of the "
+                             "interior with corner halos, ping-pong sweeps")
+            self.kname = "stencil2d_kernel<double,STENCIL9>"
+        else:
+            self.n = n or 1024
+            self.shape, self.dt, self.es = (self.n,) * 3, H.F32, 4
+            self.K, self.uses, self.part_kind = H.K_STENCIL7_3D, N7, H.ROW
+            self.modes = (5, 7, 9)
+            self.workload = (f"configs[4] (3-D half): {self.n}^3 fp32 7-point stencil (R13), slab (ROW) partition "
+                             "of the interior, ping-pong sweeps")
+            self.kname = "stencil7_kernel<float>"
+        self.dtype_name = "f64" if self.es == 8 else "f32"
+        nd = len(self.shape)
+        self.zero = [(0,) * nd]
+        self.u0 = self.initial()
+        self.X = h.create(self.dt, self.shape, self.u0)
+        self.Y = h.create(self.dt, self.shape, self.u0)
+        self.work = h.partition(self.part_kind, self.shape, (1,) * nd, tuple(s - 1 for s in self.shape))
+        self.data = h.partition(H.ROW, self.shape)
+        self.lb, self.ub = h.region(self.work, rank, nd)
+        self.my_pts = int(np.prod(np.subtract(self.ub, self.lb)))
+        self.units = int(np.prod([s - 2 for s in self.shape]))  # interior points per step
+        self.alg_per_launch = self.my_pts * 2 * self.es
+        self.src, self.dst, self.sweeps = self.X, self.Y, 0
+        self.metric_unit = "GPoints/s"
+        self.bound = "hbm"
+        self.working_set = 2 * int(np.prod(np.subtract(self.ub, self.lb) + 2)) * self.es
+
+    def initial(self):
+        if len(self.shape) == 2:
+            return synth.eigenmode2d(self.shape[0], self.shape[1], *self.modes)
+        n = self.n
+        a, b, c = self.modes
+        sz = np.sin(a * np.pi * np.arange(n) / (n - 1))
+        sy = np.sin(b * np.pi * np.arange(n) / (n - 1))
+        sx = np.sin(c * np.pi * np.arange(n) / (n - 1))
+        for v in (sz, sy, sx):
+            v[0] = v[-1] = 0.0
+        u = np.empty(self.shape, np.float32)
+        yx = np.outer(sy, sx)
+        for z in range(n):
+            u[z] = (sz[z] * yx).astype(np.float32)
+        return u
+
+    def lam(self):
+        th = [m * np.pi / (s - 1) for m, s in zip(self.modes, self.shape)]
+        if self.kind == "jacobi2d":
+            return (np.cos(th[0]) + np.cos(th[1])) / 2
+        if self.kind == "stencil9":
+            return (8 * (np.cos(th[0]) + np.cos(th[1])) + 4 * np.cos(th[0]) * np.cos(th[1])) / 20
+        return sum(np.cos(t) for t in th) / 3
+
+    def step(self):
+        self.h.apply(self.K, self.work, [(self.dst, [], self.zero), (self.src, self.uses, [])])
+        self.src, self.dst = self.dst, self.src
+        self.sweeps += 1
+
+    def reset_input(self):
+        self.src, self.dst = self.X, self.Y
+
+    def parity(self):
+        got = self.h.read(self.src, self.data)
+        d_lb, d_ub = self.h.region(self.data, self.rank, len(self.shape))
+        r0, r1 = max(self.lb[0], d_lb[0]), min(self.ub[0], d_ub[0])
+        ref = self.lam() ** self.sweeps * self.u0[r0:r1].astype(np.float64)
+        err = float(np.max(np.abs(got[r0:r1].astype(np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-300))
+        tol = 1e-12 if self.es == 8 else 1e-4
+        return {"closed_form_normwise_err": err, "tol": tol, "sweeps": self.sweeps}
+
+
+class Repartition:
+    """configs[3]: 32768^2 fp32, K1 = SCALE under ROW, K2 = SCALE under COL; every
+    switch is a full P(P-1)-block redistribution (all-to-all over NVLink)."""
+
+    def __init__(self, H, h, rank, ws, n=None):
+        self.H, self.h, self.rank, self.ws = H, h, rank, ws
+        self.n = n or 32768
+        self.shape = (self.n, self.n)
+        self.X = h.create(H.F32, self.shape)
+        self.rowp = h.partition(H.ROW, self.shape)
+        self.colp = h.partition(H.COL, self.shape)
+        self.seed = 4242
+        h.apply(H.K_STAMP, self.rowp, [(self.X, [], [(0, 0)])], [float(self.seed)])  # device-side init
+        self.kind = "repartition"
+        self.workload = (f"configs[3]: repartition ROW<->COL of a {self.n}x{self.n} fp32 array between two "
+                         "SCALE kernels (alpha=1), all-to-all over NVLink")
+        self.kname = "copy_runs_kernel (fused NVLink pull)"
+        self.dtype_name = "f32"
+        self.metric_unit = "GB/s"
+        self.bound = "nvlink" if ws > 1 else "hbm"
+        self.calls = 0
+        P = ws
+        blk = (self.n // P) * (self.n // P) * 4
+        self.units = P * (P - 1) * blk  # bytes moved by all ranks per call (one redistribution)
+        self.alg_per_launch = (P - 1) * blk  # bytes pulled by this rank per call
+        self.my_pts = 0
+        self.working_set = self.n * self.n * 4
+
+    def step(self):
+        part = self.colp if self.calls % 2 == 0 else self.rowp
+        self.h.apply(self.H.K_SCALE, part, [(self.X, [(0, 0)], [(0, 0)])], [1.0])
+        self.calls += 1
+
+    def reset_input(self):
+        pass
+
+    def parity(self):
+        # raw bits of a sampled block of this rank's rows against splitmix64 (STAMP is
+        # splitmix64(seed*phi + c)); SCALE by 1.0 keeps every non-NaN value bit-exact
+        got = self.h.read(self.X, self.rowp)
+        lb, ub = self.h.region(self.rowp, self.rank, 2)
+        r = lb[0]
+        c = np.arange(self.n, dtype=np.int64) + r * self.n
+        exp = synth.splitmix64_stream(self.seed, int(c[0]), self.n)
+        e32 = (exp & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.float32)
+        g = got[r]
+        ok = (g.view(np.uint32) == e32.view(np.uint32)) | (np.isnan(g) & np.isnan(e32))
+        return {"raw_bits_row_match": bool(ok.all()), "row": int(r)}
+
+
+class Gemm:
+    """configs[4] (product half): C = A @ B, 16384^2 bf16 in, fp32 C, ROW partition;
+    call 1 all-gathers B, steady-state calls move nothing."""
+
+    def __init__(self, H, h, rank, ws, n=None):
+        self.H, self.h, self.rank, self.ws = H, h, rank, ws
+        self.n = n or 16384
+        n = self.n
+        S = H.STAR
+        self.Ab = synth.int_bf16(51, (n, n))
+        self.Bb = synth.int_bf16(52, (n, n))
+        self.A = h.create(H.BF16, (n, n))
+        self.B = h.create(H.BF16, (n, n))
+        self.C = h.create(H.F32, (n, n))
+        self.part = h.partition(H.ROW, (n, n))
+        h.write(self.A, self.part, self.Ab)
+        h.write(self.B, self.part, self.Bb)
+        self.acc = [(self.C, [], [(0, 0)]), (self.A, [(0, S)], []), (self.B, [(S, 0)], [])]
+        self.kind = "gemm"
+        self.workload = f"configs[4] (product half): {n}^2 bf16 GEMM, fp32 accumulate and C, ROW partition, B use=all"
+        self.kname = "gemm_kernel<float> (tcgen05)"
+        self.dtype_name = "bf16"
+        self.metric_unit = "TFLOP/s"
+        self.bound = "tensor"
+        lb, ub = h.region(self.part, rank, 2)
+        self.my_rows = ub[0] - lb[0]
+        self.units = 2 * n ** 3 / 1e3  # GFLOP... scaled below
+        self.alg_per_launch = 2.0 * self.my_rows * n * n
+        self.my_pts = 0
+        self.working_set = 3 * n * n * 2
+
+    def step(self):
+        self.h.apply(self.H.K_GEMM, self.part, self.acc, [1.0, 0.0])
+
+    def reset_input(self):
+        pass
+
+    def parity(self):
+        got = self.h.read(self.C, self.part)
+        lb, ub = self.h.region(self.part, self.rank, 2)
+        rng = np.random.default_rng(7)
+        ii = rng.integers(lb[0], ub[0], 64)
+        jj = rng.integers(0, self.n, 64)
+        A = synth.bf16_to_f32(self.Ab[ii]).astype(np.int64)
+        exact = np.einsum("sk,ks->s", A, synth.bf16_to_f32(self.Bb[:, jj]).astype(np.int64))
+        return {"integer_exact_samples": bool((got[ii, jj].astype(np.int64) == exact).all()), "samples": 64}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="hdarray")
-    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--workload", default="jacobi2d",
+                    choices=["jacobi2d", "stencil9", "stencil7", "repartition", "gemm"])
+    ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--e2e-sweeps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", type=int, default=0)
+    ap.add_argument("--no-overlap", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
+    defaults = {"jacobi2d": (1000, 20), "stencil9": (200, 10), "stencil7": (100, 5), "repartition": (40, 4),
+                "gemm": (20, 3)}[args.workload]
+    args.steps = args.steps or defaults[0]
+    args.warmup = max(args.warmup if args.warmup is not None else defaults[1], 3)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -182,40 +383,26 @@ def main():
     import torch.distributed as dist
 
     import paper_1809_05657_b200 as H
-    import synth
 
     ws, rank, local = dist_env()
-    if ws != args.gpus:
-        args.gpus = ws
+    args.gpus = ws
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     hbm_peak, peak_src = peaks()
-
-    n = args.n
-    P = ws
     if ws > 1:
-        h = H.HDArray.spmd(P, rank, local)
+        h = H.HDArray.spmd(ws, rank, local)
     else:
         h = H.HDArray(n_gpus=1, n_devices=1, gpu_ids=[local])
     h.set_transport(args.transport)
-    a_mode, b_mode = 37, 61
-    u0 = synth.eigenmode2d(n, n, a_mode, b_mode)
-    X = h.create(H.F64, (n, n), u0)
-    Y = h.create(H.F64, (n, n), u0)
-    work = h.partition(H.ROW, (n, n), (1, 1), (n - 1, n - 1))
-    data = h.partition(H.ROW, (n, n))
-    my_lb, my_ub = h.region(work, rank, 2)
-    my_pts = (my_ub[0] - my_lb[0]) * (my_ub[1] - my_lb[1])
-    total_pts = (n - 2) * (n - 2)
+    h.set_overlap(not args.no_overlap)
+    if args.workload in ("jacobi2d", "stencil9", "stencil7"):
+        wl = Stencil(args.workload, H, h, rank, ws, args.n)
+    elif args.workload == "repartition":
+        wl = Repartition(H, h, rank, ws, args.n)
+    else:
+        wl = Gemm(H, h, rank, ws, args.n)
     stream = torch.cuda.ExternalStream(h.stream(rank))
-    sweeps_done = [0]
-    state = {"src": X, "dst": Y}
-
-    def step():
-        h.apply(H.K_JACOBI5, work, [(state["dst"], [], [(0, 0)]), (state["src"], J, [])])
-        state["src"], state["dst"] = state["dst"], state["src"]
-        sweeps_done[0] += 1
 
     def barrier():
         h.sync()
@@ -223,28 +410,23 @@ def main():
         if ws > 1:
             dist.barrier()
 
-    def max_over_ranks(x):
+    def reduce(x, op):
         if ws == 1:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def sum_over_ranks(x):
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+    MAX = dist.ReduceOp.MAX if ws > 1 else None
+    SUM = dist.ReduceOp.SUM if ws > 1 else None
 
     # L2 policy: inputs larger than L2 => back-to-back steps; otherwise flush between steps
     l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
-    work_set = 2 * (my_ub[0] - my_lb[0] + 2) * n * 8
-    flush = work_set < 2 * l2_bytes
+    flush = wl.working_set < 2 * l2_bytes
     flush_buf = torch.empty(int(2 * l2_bytes), dtype=torch.uint8, device="cuda") if flush else None
 
     for _ in range(args.warmup):
-        step()
+        wl.step()
     barrier()
     h.reset_stats()
 
@@ -259,12 +441,11 @@ def main():
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            wl.step()
         ev1.record(stream)
         barrier()
         ms = ev0.elapsed_time(ev1)
     else:
-        ms = 0.0
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         barrier()
         for i in range(args.steps):
@@ -274,96 +455,120 @@ def main():
                 torch.cuda.synchronize()
                 dist.barrier()
             evs[i][0].record(stream)
-            step()
+            wl.step()
             evs[i][1].record(stream)
         barrier()
         ms = sum(a.elapsed_time(b) for a, b in evs)
     launches = h.stats()["kernel_launches"] - launches0
     clocks = clk.stop()
     st = h.stats()
-    ms = max_over_ranks(ms)
-    value = total_pts * args.steps / (ms * 1e-3) / 1e9
+    ms = reduce(ms, MAX)
+    if wl.metric_unit == "GPoints/s":
+        value = wl.units * args.steps / (ms * 1e-3) / 1e9
+    elif wl.metric_unit == "GB/s":
+        value = wl.units * args.steps / (ms * 1e-3) / 1e9
+    else:
+        value = 2.0 * wl.n ** 3 * args.steps / (ms * 1e-3) / 1e12
 
     # ---- per-kernel timing pass (CUDA events bracketing each launch on its stream)
     h.set_kernel_timing(True)
     h.reset_stats()
     kt_steps = min(args.steps, 200)
     for _ in range(kt_steps):
-        step()
+        wl.step()
     barrier()
-    k_ms, k_n = h.kernel_time(H.K_JACOBI5)
+    kid = {"jacobi2d": H.K_JACOBI5, "stencil9": H.K_STENCIL9, "stencil7": H.K_STENCIL7_3D,
+           "repartition": H.K_SCALE, "gemm": H.K_GEMM}[args.workload]
+    k_ms, k_n = h.kernel_time(kid)
     x_ms, x_n = h.exchange_time()
     st_kt = h.stats()
     h.set_kernel_timing(False)
     k_avg = k_ms / max(k_n, 1)
-    achieved = my_pts * 16 / (k_avg * 1e-3) / 1e9  # algorithmic bytes: 8 B read + 8 B write per point
-    achieved = min(achieved, sum_over_ranks(achieved) / ws) if ws > 1 else achieved
-    halo_bytes = st_kt["bytes_total"] / max(kt_steps, 1)
     x_avg = x_ms / max(x_n, 1)
+    halo_bytes = st_kt["bytes_total"] / max(kt_steps, 1)
+    if wl.bound == "hbm" and args.workload != "repartition":
+        achieved = wl.alg_per_launch / (k_avg * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": wl.kname, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": wl.alg_per_launch, "avg_launch_ms": k_avg}
+    elif args.workload == "repartition":
+        if ws > 1:
+            achieved = wl.alg_per_launch / (x_avg * 1e-3) / 1e9  # bytes received per GPU / pull time
+            roof = {"bound": "nvlink", "kernel": wl.kname, "achieved": achieved, "peak": NVLINK_GBS,
+                    "unit": "GB/s", "frac": achieved / NVLINK_GBS,
+                    "peak_source": "measured peer copy per direction (B200_PROFILING.md); 900 nominal",
+                    "algorithmic_bytes_per_launch": wl.alg_per_launch, "avg_launch_ms": x_avg}
+        else:
+            scale_bytes = wl.n * wl.n * 4 * 2
+            achieved = scale_bytes / (k_avg * 1e-3) / 1e9
+            roof = {"bound": "hbm", "kernel": "scale_kernel<float>", "achieved": achieved, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": scale_bytes, "avg_launch_ms": k_avg}
+    else:
+        sustained = 1399.6
+        try:
+            sustained = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"])
+        except Exception:
+            pass
+        achieved = wl.alg_per_launch / (k_avg * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": wl.kname, "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+                "frac": achieved / sustained, "peak_source": "measured cuBLAS bf16 sustained (MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_launch": wl.alg_per_launch, "avg_launch_ms": k_avg}
+    if ws > 1:
+        roof["achieved_min_over_ranks"] = -reduce(-roof["achieved"], MAX)
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    roof["traffic"] = None
+    if os.path.exists(tp):
+        try:
+            roof["traffic"] = json.load(open(tp)).get(f"{args.workload}_n{wl.n}_P{ws}")
+        except Exception:
+            pass
 
-    # ---- parity against the closed form (eigenmode) on this rank's rows
-    lam = (np.cos(a_mode * np.pi / (n - 1)) + np.cos(b_mode * np.pi / (n - 1))) / 2
-    got = h.read(state["src"], data)
-    d_lb, d_ub = h.region(data, rank, 2)
-    rows = slice(max(my_lb[0], d_lb[0]), min(my_ub[0], d_ub[0]))
-    ref = lam ** sweeps_done[0] * u0[rows]
-    err = float(np.max(np.abs(got[rows] - ref)) / np.max(np.abs(ref)))
-    err = max_over_ranks(err)
+    par = wl.parity()
 
-    # ---- end to end through the C-ABI with host buffers: write (pinned H2D) ->
-    # e2e_sweeps sweeps -> read (D2H) per job
-    host_in = torch.from_numpy(u0).pin_memory()
-    host_out = torch.empty((n, n), dtype=torch.float64).pin_memory()
-    jobs = 2
-    e2e_times = []
-    for j in range(jobs + 1):
-        barrier()
-        t0 = time.perf_counter()
-        h.write_ptr(X, data, host_in.data_ptr())
-        state["src"], state["dst"] = X, Y
-        for _ in range(args.e2e_sweeps):
-            step()
-        h.read_ptr(state["src"], data, host_out.data_ptr())
-        barrier()
-        if j:
-            e2e_times.append(time.perf_counter() - t0)
-    e2e_s = max_over_ranks(min(e2e_times))
-    my_rows = my_ub[0] - my_lb[0] + (1 if rank == 0 else 0) + (1 if rank == ws - 1 else 0)
-    e2e = {"value": total_pts * args.e2e_sweeps / e2e_s / 1e9, "unit": "GPoints/s",
-           "h2d_bytes_per_step": int(sum_over_ranks(my_rows * n * 8)),
-           "d2h_bytes_per_step": int(sum_over_ranks(my_rows * n * 8)),
-           "step": f"one configs[1] job: hda_write X -> {args.e2e_sweeps} sweeps -> hda_read (host wall clock)"}
+    # ---- end to end through the C-ABI with host buffers (stencils: write (pinned H2D)
+    # -> e2e_sweeps sweeps -> read (D2H) per job)
+    e2e = None
+    if not args.no_e2e and isinstance(wl, Stencil):
+        host_in = torch.from_numpy(np.ascontiguousarray(wl.u0)).pin_memory()
+        host_out = torch.empty(wl.shape, dtype=host_in.dtype).pin_memory()
+        times = []
+        for j in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            h.write_ptr(wl.X, wl.data, host_in.data_ptr())
+            wl.reset_input()
+            for _ in range(args.e2e_sweeps):
+                wl.step()
+            h.read_ptr(wl.src, wl.data, host_out.data_ptr())
+            barrier()
+            if j:
+                times.append(time.perf_counter() - t0)
+        e2e_s = reduce(min(times), MAX)
+        d_lb, d_ub = h.region(wl.data, rank, len(wl.shape))
+        my_bytes = int(np.prod(np.subtract(d_ub, d_lb))) * wl.es
+        e2e = {"value": wl.units * args.e2e_sweeps / e2e_s / 1e9, "unit": "GPoints/s",
+               "h2d_bytes_per_step": int(reduce(my_bytes, SUM)), "d2h_bytes_per_step": int(reduce(my_bytes, SUM)),
+               "step": f"one job: hda_write -> {args.e2e_sweeps} sweeps -> hda_read (host wall clock, pinned)"}
 
-    launches = int(sum_over_ranks(launches))
+    launches = int(reduce(launches, SUM))
     if rank == 0:
         cpu = None
-        if ws == 1 and not args.no_cpu_baseline:
+        if ws == 1 and not args.no_cpu_baseline and args.workload == "jacobi2d":
             cpu = oracle_sample()
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get(f"jacobi5_f64_n{n}_P{ws}")
-            except Exception:
-                traffic = None
         line = {
-            "metric": METRIC, "value": value, "unit": "GPoints/s", "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": wl.metric_unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1]: 8192x8192 fp64 Jacobi (P:L459), ROW partition of the interior, "
-                                   "ping-pong sweeps through hda_apply", "n": n, "global_points": total_pts,
-                       "parallelism": f"spmd{ws}" if ws > 1 else "single",
-                       "transport": ["fused", "staged"][args.transport],
+            "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype_name, "data": "synthetic",
+            "config": {"workload": wl.workload, "n": wl.n, "parallelism": f"spmd{ws}" if ws > 1 else "single",
+                       "transport": ["fused", "staged"][args.transport], "overlap": not args.no_overlap,
                        "l2": ("L2 flushed between timed steps" if flush else
-                              f"inputs larger than L2 (per-GPU working set {work_set / 2**20:.0f} MiB)")},
-            "roofline": {"bound": "hbm", "kernel": "stencil2d_kernel<double,JACOBI5>",
-                         "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": my_pts * 16, "avg_launch_ms": k_avg},
-            "exchange": {"halo_bytes_per_step": halo_bytes, "exchange_ms_per_step": x_avg if x_n else 0.0,
-                         "halo_GBps_per_gpu": (halo_bytes / ws / (x_avg * 1e-3) / 1e9) if x_n else None,
+                              f"inputs larger than L2 (per-GPU working set {wl.working_set / 2**20:.0f} MiB)")},
+            "roofline": roof,
+            "exchange": {"bytes_per_step": halo_bytes, "exchange_ms_per_step": x_avg if x_n else 0.0,
+                         "GBps_per_gpu": (halo_bytes / ws / (x_avg * 1e-3) / 1e9) if x_n else None,
                          "nvlink_peak_GBps": NVLINK_GBS},
-            "parity": {"closed_form_normwise_err": err, "tol": 1e-12, "pass": err < 1e-12},
+            "parity": par,
             "tracker": {"plan_hits": st["plan_hits"], "plan_misses": st["plan_misses"],
                         "tracker_us_per_call": st["tracker_us"] / max(st["n_apply"], 1)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,

@@ -229,6 +229,10 @@ int hda_read(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, void* host_full);
 
 /* ---- transport / tuning ---- */
 int hda_set_transport(hda_ctx_t* ctx, int32_t transport);
+/* overlap on/off (default on): when a device's halo comes from another GPU, its pull
+ * runs on a second stream while the kernel computes the part of the work box whose
+ * footprint touches no incoming rectangle; the rest runs after the pull lands. */
+int hda_set_overlap(hda_ctx_t* ctx, int32_t enabled);
 /* plan cache on/off (off => every call recomputes the plan; used to time the
  * baseline of P:L502 and to test cache transparency) */
 int hda_set_plan_cache(hda_ctx_t* ctx, int32_t enabled);

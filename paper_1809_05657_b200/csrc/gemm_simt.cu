@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.cuh"
+#include "sync.cuh"
 
 namespace hda {
 
@@ -24,7 +25,8 @@ template <typename TC>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const __nv_bfloat16* __restrict__ A,
                                                         const __nv_bfloat16* __restrict__ B, TC* C, int64_t N,
                                                         int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1,
-                                                        float alpha, float beta) {
+                                                        float alpha, float beta, const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   __shared__ float As[32][65];
   __shared__ float Bs[32][65];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -66,20 +68,22 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const __nv_bfloat16* __r
         st_c<TC>(p, v);
       }
     }
+  ks_post(ks);
 }
 
 cudaError_t launch_gemm_simt(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
-                             const int64_t* lb, const int64_t* ub, float alpha, float beta, cudaStream_t s) {
+                             const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
+                             cudaStream_t s) {
   (void)M;
   const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
   if (m0 >= m1 || n0 >= n1) return cudaSuccess;
   dim3 grid((unsigned)((n1 - n0 + 63) / 64), (unsigned)((m1 - m0 + 63) / 64));
   if (c_dtype == 1)
     gemm_simt_kernel<float><<<grid, 256, 0, s>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B, (float*)C, N, K,
-                                                 m0, m1, n0, n1, alpha, beta);
+                                                 m0, m1, n0, n1, alpha, beta, ks);
   else
     gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)A, (const __nv_bfloat16*)B,
-                                                         (__nv_bfloat16*)C, N, K, m0, m1, n0, n1, alpha, beta);
+                                                         (__nv_bfloat16*)C, N, K, m0, m1, n0, n1, alpha, beta, ks);
   return cudaGetLastError();
 }
 

@@ -20,11 +20,13 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "sync.cuh"
 
 namespace hda {
 
 cudaError_t launch_gemm_simt(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
-                             const int64_t* lb, const int64_t* ub, float alpha, float beta, cudaStream_t s);
+                             const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
+                             cudaStream_t s);
 
 namespace tc {
 
@@ -198,7 +200,9 @@ __device__ __forceinline__ void store_chunk<__nv_bfloat16>(__nv_bfloat16* row, i
 template <typename TC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, TC* C,
-                int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, float alpha, float beta) {
+                int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, float alpha, float beta,
+                const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
   }
+  ks_post(ks);
 }
 
 // ---------------------------------------------------------------- host side
@@ -374,7 +379,8 @@ static int sm_count() {
 }
 
 cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
-                        const int64_t* lb, const int64_t* ub, float alpha, float beta, cudaStream_t s) {
+                        const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
+                        cudaStream_t s) {
   const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
   if (m0 >= m1 || n0 >= n1) return cudaSuccess;
   // TMA needs 16-byte row pitches and aligned bases; tiny problems use the CUDA-core path
@@ -383,18 +389,18 @@ cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int6
   CUtensorMap ma, mb;
   if (!tc_ok || !tc::make_map(&ma, A, (uint64_t)K, (uint64_t)M, tc::BM) ||
       !tc::make_map(&mb, B, (uint64_t)N, (uint64_t)K, tc::BK))
-    return launch_gemm_simt(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, s);
+    return launch_gemm_simt(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, ks, s);
   const int64_t tiles = ((m1 - m0 + tc::BM - 1) / tc::BM) * ((n1 - n0 + tc::BN - 1) / tc::BN);
   const int grid = (int)std::min<int64_t>(tiles, sm_count());
   if (c_dtype == 1) {
     cudaFuncSetAttribute(tc::gemm_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
     tc::gemm_kernel<float><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(ma, mb, (float*)C, N, K, m0, m1, n0, n1, alpha,
-                                                                     beta);
+                                                                     beta, ks);
   } else {
     cudaFuncSetAttribute(tc::gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          tc::SMEM_BYTES);
     tc::gemm_kernel<__nv_bfloat16><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(ma, mb, (__nv_bfloat16*)C, N, K, m0,
-                                                                             m1, n0, n1, alpha, beta);
+                                                                             m1, n0, n1, alpha, beta, ks);
   }
   return cudaGetLastError();
 }

@@ -39,12 +39,14 @@ using namespace hda;
 
 namespace {
 
-constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_WORDS = 192;
+constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_CTR_PULL = 192, SW_CTR_KERN = 193, SW_WORDS = 256;
 constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
 
 struct Gpu {
   int ordinal = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;  // compute (and everything else)
+  cudaStream_t comm = nullptr;    // overlapped halo pulls
+  cudaEvent_t ev_fork = nullptr, ev_pull = nullptr;
 };
 
 struct Dev {
@@ -64,6 +66,7 @@ struct ArrRT {
 struct TimedEv {
   int kind;  // kernel id, or -100 for exchange
   cudaEvent_t a, b;
+  int count;  // 1 for the first launch of a call, 0 for its continuation launches
 };
 
 struct PullJob {
@@ -71,6 +74,11 @@ struct PullJob {
   std::vector<int> srcs;
   std::vector<RunBatch> batches;
   std::vector<std::pair<int, int>> pend;  // (array, src) pairs read by this pull
+  bool cross = false;                     // some source lives on another stream/GPU
+  // overlap split of the reader's work box: cells whose footprint does not touch any
+  // incoming rectangle (run while the pull is in flight) and the rest (after it)
+  bool split = false;
+  std::vector<Box> interior, dependent;
 };
 struct PackJob {
   int src;
@@ -114,7 +122,9 @@ struct hda_ctx {
   std::vector<size_t> send_cap, recv_cap;
   std::unordered_map<uint64_t, ExecPlan> exec;
   int transport = HDA_XPORT_FUSED;
-  bool cache_on = true, ktiming = false;
+  bool cache_on = true, ktiming = false, overlap = true;
+  std::vector<char> pulled_on_comm;  // [P] this call's pull for device q ran on the comm stream
+  std::vector<const PullJob*> cur_pull;
   std::vector<TimedEv> tev;
   std::vector<cudaEvent_t> ev_pool;
   double ktime_ms[KN_COUNT] = {};
@@ -216,12 +226,15 @@ static RunDesc rect_desc(const int64_t* S, const Box& fb, size_t es) {
 static void batch_descs(std::vector<RunDesc>& descs, std::vector<RunBatch>& out) {
   RunBatch b;
   std::memset(&b, 0, sizeof b);
+  int64_t total = 0;
+  for (const RunDesc& d : descs) total += d.run_bytes * d.n0 * d.n1;
+  const int64_t chunk = pick_chunk_bytes(total);
   for (RunDesc d : descs) {
     if (b.n == kMaxRunDescs) {
       out.push_back(b);
       std::memset(&b, 0, sizeof b);
     }
-    int64_t u = run_desc_units(d);
+    int64_t u = run_desc_units(d, chunk);
     if (u == 0) continue;
     d.unit_begin = b.total_units;
     b.total_units += u;
@@ -267,6 +280,28 @@ static void wl_add(WaitList& w, unsigned long long* p, unsigned long long v) {
   w.n++;
 }
 
+static KSync ks_empty(hda_ctx_t* ctx) {
+  KSync k;
+  k.nwait = 0;
+  k.nsig = 0;
+  k.sig_val = 0;
+  k.ctr = nullptr;
+  k.err = ctx->err_host;
+  k.timeout_ns = ctx->timeout_ns;
+  return k;
+}
+static void ks_wait(KSync& k, unsigned long long* p, unsigned long long v) {
+  if (v == 0) return;
+  for (int i = 0; i < k.nwait; i++)
+    if (k.wait_ptr[i] == p) {
+      if (k.wait_val[i] < v) k.wait_val[i] = v;
+      return;
+    }
+  k.wait_ptr[k.nwait] = p;
+  k.wait_val[k.nwait] = v;
+  k.nwait++;
+}
+
 static int check_err_flag(hda_ctx_t* ctx) {
   if (ctx->err_host && *(volatile int*)ctx->err_host) {
     ctx->sticky = HDA_ETIMEOUT;
@@ -279,6 +314,7 @@ static int check_err_flag(hda_ctx_t* ctx) {
 static int sync_all(hda_ctx_t* ctx) {
   for (auto& g : ctx->gpus) {
     CK(cudaSetDevice(g.ordinal));
+    CK(cudaStreamSynchronize(g.comm));
     CK(cudaStreamSynchronize(g.stream));
   }
   return check_err_flag(ctx);
@@ -323,6 +359,32 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
       }
       if (descs.empty()) continue;
       batch_descs(descs, job.batches);
+      for (int p : job.srcs)
+        if (!same_stream(ctx, p, q)) job.cross = true;
+      // overlap split (footprint radius r of the built-in kernel)
+      const CallInfo& ci = *t->info;
+      int r = -1;
+      if (ci.kernel == KN_JACOBI5 || ci.kernel == KN_STENCIL9 || ci.kernel == KN_STENCIL7_3D) r = 1;
+      if (ci.kernel == KN_SCALE || ci.kernel == KN_COPY) r = 0;
+      const Box& w = ctx->tr->part(ci.part).box[q];
+      if (r >= 0 && !box_empty(w)) {
+        const int nd = ctx->tr->part(ci.part).ndim;
+        std::vector<Box> dil;
+        for (const Msg& m : t->msgs) {
+          if (m.dst != q) continue;
+          Box b = m.box;
+          for (int kk = 0; kk < nd; kk++) {
+            b.lb[kk] -= r;
+            b.ub[kk] += r;
+          }
+          dil.push_back(b);
+        }
+        Rects W{w};
+        Rects D = intersect(W, canonicalize(dil));
+        job.dependent = D;
+        job.interior = subtract(W, D);
+        job.split = true;
+      }
       ep.pulls.push_back(std::move(job));
     }
     return HDA_OK;
@@ -416,22 +478,22 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
 
 // ====================================================================== phases
 
-static int timed_begin(hda_ctx_t* ctx, int d, cudaEvent_t* a) {
+static int timed_begin(hda_ctx_t* ctx, cudaStream_t st, cudaEvent_t* a) {
   *a = nullptr;
   if (!ctx->ktiming) return HDA_OK;
   *a = get_event(ctx);
-  CK(cudaEventRecord(*a, stream_of(ctx, d)));
+  CK(cudaEventRecord(*a, st));
   return HDA_OK;
 }
-static int timed_end(hda_ctx_t* ctx, int d, int kind, cudaEvent_t a) {
+static int timed_end(hda_ctx_t* ctx, cudaStream_t st, int kind, cudaEvent_t a, int count = 1) {
   if (!a) return HDA_OK;
   cudaEvent_t b = get_event(ctx);
-  CK(cudaEventRecord(b, stream_of(ctx, d)));
-  ctx->tev.push_back(TimedEv{kind, a, b});
+  CK(cudaEventRecord(b, st));
+  ctx->tev.push_back(TimedEv{kind, a, b, count});
   return HDA_OK;
 }
 
-static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k) {
+static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k, bool overlap_kernel) {
   if (t->msgs.empty()) return HDA_OK;
   ExecPlan* ep;
   ExecPlan scratch;
@@ -454,26 +516,46 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
     for (PullJob& job : ep->pulls) {
       const int q = job.dst;
       CK(cudaSetDevice(ordinal_of(ctx, q)));
-      WaitList wl;
-      wl.n = 0;
-      SignalList sl;
-      sl.n = 0;
-      sl.val = k;
+      Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+      const bool comm = ctx->overlap && job.cross && job.split && overlap_kernel;
+      cudaStream_t st = comm ? g.comm : g.stream;
+      if (comm) {  // the pull may start as soon as everything issued before this call is done
+        CK(cudaEventRecord(g.ev_fork, g.stream));
+        CK(cudaStreamWaitEvent(g.comm, g.ev_fork, 0));
+        ctx->pulled_on_comm[q] = 1;
+        ctx->cur_pull[q] = &job;
+      }
+      // RAW waits and ACK signals ride in the pull kernel itself (sync.cuh)
+      KSync pre = ks_empty(ctx), post = ks_empty(ctx);
+      post.sig_val = k;
+      post.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
       for (int p : job.srcs)
         if (!same_stream(ctx, p, q)) {
-          wl_add(wl, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
-          sl.ptr[sl.n++] = ctx->dev[p].sync + SW_ACK + q;
+          ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
+          post.sig_ptr[post.nsig++] = ctx->dev[p].sync + SW_ACK + q;
         }
-      int rc = launch_waits(ctx, q, wl);
-      if (rc) return rc;
+      int rc;
       cudaEvent_t a;
-      if ((rc = timed_begin(ctx, q, &a))) return rc;
-      for (const RunBatch& b : job.batches) {
-        CK(launch_copy_runs(b, stream_of(ctx, q)));
+      if ((rc = timed_begin(ctx, st, &a))) return rc;
+      const size_t nb = job.batches.size();
+      for (size_t i = 0; i < nb; i++) {
+        KSync ks = ks_empty(ctx);
+        if (i == 0) {
+          std::memcpy(ks.wait_ptr, pre.wait_ptr, sizeof ks.wait_ptr);
+          std::memcpy(ks.wait_val, pre.wait_val, sizeof ks.wait_val);
+          ks.nwait = pre.nwait;
+        }
+        if (i + 1 == nb) {
+          std::memcpy(ks.sig_ptr, post.sig_ptr, sizeof ks.sig_ptr);
+          ks.nsig = post.nsig;
+          ks.sig_val = post.sig_val;
+          ks.ctr = post.ctr;
+        }
+        CK(launch_copy_runs(job.batches[i], ks, st));
         count_launch(ctx);
       }
-      if ((rc = timed_end(ctx, q, -100, a))) return rc;
-      if ((rc = launch_signals(ctx, q, sl))) return rc;
+      if ((rc = timed_end(ctx, st, -100, a))) return rc;
+      if (comm) CK(cudaEventRecord(g.ev_pull, g.comm));
       for (auto& pr : job.pend) ctx->pend[pr.first][pr.second][q] = k;
     }
     return HDA_OK;
@@ -490,12 +572,12 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
     int rc = launch_waits(ctx, p, wl);
     if (rc) return rc;
     cudaEvent_t a;
-    if ((rc = timed_begin(ctx, p, &a))) return rc;
+    if ((rc = timed_begin(ctx, stream_of(ctx, p), &a))) return rc;
     for (const RunBatch& b : job.batches) {
-      CK(launch_copy_runs(b, stream_of(ctx, p)));
+      CK(launch_copy_runs(b, ks_empty(ctx), stream_of(ctx, p)));
       count_launch(ctx);
     }
-    if ((rc = timed_end(ctx, p, -100, a))) return rc;
+    if ((rc = timed_end(ctx, stream_of(ctx, p), -100, a))) return rc;
     SignalList sl;
     sl.n = 0;
     sl.val = k;
@@ -519,64 +601,72 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
     int rc = launch_waits(ctx, q, wl);
     if (rc) return rc;
     cudaEvent_t a;
-    if ((rc = timed_begin(ctx, q, &a))) return rc;
+    if ((rc = timed_begin(ctx, stream_of(ctx, q), &a))) return rc;
     for (const Seg& s : job.segs)
       CK(cudaMemcpyAsync(ctx->recv_stage[q] + s.dst_off, ctx->send_stage[s.src] + s.src_off, s.bytes,
                          cudaMemcpyDeviceToDevice, stream_of(ctx, q)));
     for (const RunBatch& b : job.unpack) {
-      CK(launch_copy_runs(b, stream_of(ctx, q)));
+      CK(launch_copy_runs(b, ks_empty(ctx), stream_of(ctx, q)));
       count_launch(ctx);
     }
-    if ((rc = timed_end(ctx, q, -100, a))) return rc;
+    if ((rc = timed_end(ctx, stream_of(ctx, q), -100, a))) return rc;
     if ((rc = launch_signals(ctx, q, sl))) return rc;
     for (int p : job.srcs) ctx->stage_pend[p].push_back({q, k});
   }
   return HDA_OK;
 }
 
-// WAR before device q overwrites cells of the arrays it defines
-static int war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q) {
-  WaitList wl;
-  wl.n = 0;
+// WAR before device q overwrites cells of the arrays it defines: every peer that
+// pulled those arrays from q must have acknowledged the pull
+static void war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q, KSync& ks) {
   for (size_t i = 0; i < ci.arrays.size(); i++) {
     if (ci.ldef[i][q].empty()) continue;
     auto& row = ctx->pend[ci.arrays[i]][q];
     for (int r = 0; r < ctx->P; r++) {
-      if (row[r] && !same_stream(ctx, q, r)) wl_add(wl, ctx->dev[q].sync + SW_ACK + r, row[r]);
+      if (row[r] && !same_stream(ctx, q, r)) ks_wait(ks, ctx->dev[q].sync + SW_ACK + r, row[r]);
       row[r] = 0;
     }
   }
-  return launch_waits(ctx, q, wl);
 }
 
-static int signal_prod(hda_ctx_t* ctx, int q, unsigned long long k) {
-  SignalList sl;
-  sl.n = 0;
-  sl.val = k;
+// RAW: publish "device q completed call k" to every peer
+static void signal_prod(hda_ctx_t* ctx, int q, unsigned long long k, KSync& ks) {
+  ks.sig_val = k;
+  ks.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_KERN);
   for (int r = 0; r < ctx->P; r++)
-    if (r != q && !same_stream(ctx, q, r)) sl.ptr[sl.n++] = ctx->dev[r].sync + SW_PROD + q;
-  return launch_signals(ctx, q, sl);
+    if (r != q && !same_stream(ctx, q, r)) ks.sig_ptr[ks.nsig++] = ctx->dev[r].sync + SW_PROD + q;
 }
 
-static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars) {
+// separate wait/signal kernels, for phases that launch no kernel of their own
+static int sync_only(hda_ctx_t* ctx, int q, const KSync& ks) {
+  if (ks.nwait == 0 && ks.nsig == 0) return HDA_OK;
+  RunBatch empty;
+  std::memset(&empty, 0, sizeof empty);
+  CK(launch_copy_runs(empty, ks, stream_of(ctx, q)));
+  count_launch(ctx);
+  return HDA_OK;
+}
+
+static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
+                      const Box* wbox = nullptr) {
   const CallInfo& ci = *t->info;
   const TPart& pt = ctx->tr->part(ci.part);
   const int X0 = ci.param_array[0];
   const TArray& a0 = ctx->tr->array(X0);
   int64_t S[3];
   front_shape(a0.ndim, a0.shape, S);
-  const Box fb = front_box(a0.ndim, pt.box[q]);
+  const Box fb = front_box(a0.ndim, wbox ? *wbox : pt.box[q]);
   cudaStream_t s = stream_of(ctx, q);
   auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
   switch (ci.kernel) {
     case KN_JACOBI5:
-      CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, s));
+      CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, ks, s));
       break;
     case KN_STENCIL9:
-      CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, s));
+      CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, ks, s));
       break;
     case KN_STENCIL7_3D:
-      CK(launch_stencil7(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, s));
+      CK(launch_stencil7(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, ks, s));
       break;
     case KN_COPY: {
       RunDesc d = rect_desc(S, fb, a0.es);
@@ -585,11 +675,17 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
       std::vector<RunDesc> v{d};
       std::vector<RunBatch> bs;
       batch_descs(v, bs);
-      for (auto& b : bs) CK(launch_copy_runs(b, s));
+      if (bs.size() == 1) {
+        CK(launch_copy_runs(bs[0], ks, s));
+      } else {
+        for (auto& b : bs) CK(launch_copy_runs(b, ks_empty(ctx), s));
+        int rc = sync_only(ctx, q, ks);
+        if (rc) return rc;
+      }
       break;
     }
     case KN_SCALE:
-      CK(launch_scale(a0.dtype, P_(0), S, fb.lb, fb.ub, scalars[0], s));
+      CK(launch_scale(a0.dtype, P_(0), S, fb.lb, fb.ub, scalars[0], ks, s));
       break;
     case KN_STAMP: {
       const Rects& D = ci.ldef[0][q];
@@ -604,7 +700,20 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
           }
           bl.n++;
         }
-        CK(launch_stamp((int)a0.es, P_(0), S, bl, (unsigned long long)scalars[0], s));
+        // waits ride with the first launch, signals with the last
+        KSync k2 = ks_empty(ctx);
+        if (i == 0) {
+          std::memcpy(k2.wait_ptr, ks.wait_ptr, sizeof k2.wait_ptr);
+          std::memcpy(k2.wait_val, ks.wait_val, sizeof k2.wait_val);
+          k2.nwait = ks.nwait;
+        }
+        if (i + 16 >= D.size()) {
+          std::memcpy(k2.sig_ptr, ks.sig_ptr, sizeof k2.sig_ptr);
+          k2.nsig = ks.nsig;
+          k2.sig_val = ks.sig_val;
+          k2.ctr = ks.ctr;
+        }
+        CK(launch_stamp((int)a0.es, P_(0), S, bl, (unsigned long long)scalars[0], k2, s));
       }
       break;
     }
@@ -612,7 +721,7 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
       const TArray& A = ctx->tr->array(ci.param_array[1]);
       const TArray& B = ctx->tr->array(ci.param_array[2]);
       CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], A.shape[1], fb.lb, fb.ub,
-                     (float)scalars[0], (float)scalars[1], s));
+                     (float)scalars[0], (float)scalars[1], ks, s));
       break;
     }
     default:
@@ -673,7 +782,9 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
   const unsigned long long k = ++ctx->epoch;
   if (!ctx->plan_only) {
     DevGuard g(true);
-    if ((rc = do_exchange(ctx, t, k))) return rc;
+    const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
+                                kernel == KN_SCALE || kernel == KN_COPY;
+    if ((rc = do_exchange(ctx, t, k, overlap_kernel))) return rc;
     const TPart& pt = ctx->tr->part(part);
     for (int q = 0; q < ctx->P; q++) {
       if (!ctx->dev[q].local) continue;
@@ -685,10 +796,24 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
       const bool io = (kernel == KN_WRITE && has_work) || (kernel == KN_READ && has_work);
       if (!defines && !kern && !io) continue;
       CK(cudaSetDevice(ordinal_of(ctx, q)));
-      if (defines && (rc = war_waits(ctx, ci, q))) return rc;
+      KSync ks = ks_empty(ctx);
+      if (defines) {
+        war_waits(ctx, ci, q, ks);
+        signal_prod(ctx, q, k, ks);
+      }
       const int X0 = ci.param_array[0];
       const TArray& a0 = ctx->tr->array(X0);
       if (io) {
+        // host copies cannot carry sync words: separate wait before, signal after
+        KSync pre = ks_empty(ctx), post = ks_empty(ctx);
+        std::memcpy(pre.wait_ptr, ks.wait_ptr, sizeof pre.wait_ptr);
+        std::memcpy(pre.wait_val, ks.wait_val, sizeof pre.wait_val);
+        pre.nwait = ks.nwait;
+        std::memcpy(post.sig_ptr, ks.sig_ptr, sizeof post.sig_ptr);
+        post.nsig = ks.nsig;
+        post.sig_val = ks.sig_val;
+        post.ctr = ks.ctr;
+        if ((rc = sync_only(ctx, q, pre))) return rc;
         int64_t S[3];
         front_shape(a0.ndim, a0.shape, S);
         Box fb = front_box(a0.ndim, pt.box[q]);
@@ -715,15 +840,56 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
           p.kind = cudaMemcpyDeviceToHost;
         }
         if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
+        if ((rc = sync_only(ctx, q, post))) return rc;
+      } else if (kern && ctx->pulled_on_comm[q]) {
+        // interior boxes while the pull is in flight, dependent boxes after it
+        const PullJob& job = *ctx->cur_pull[q];
+        Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+        std::vector<std::pair<const Box*, bool>> seq;  // (box, after the pull)
+        for (const Box& b : job.interior) seq.push_back({&b, false});
+        for (const Box& b : job.dependent) seq.push_back({&b, true});
+        bool joined = false;
+        for (size_t i = 0; i < seq.size(); i++) {
+          if (seq[i].second && !joined) {
+            CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+            joined = true;
+          }
+          KSync k2 = ks_empty(ctx);
+          if (i == 0) {
+            std::memcpy(k2.wait_ptr, ks.wait_ptr, sizeof k2.wait_ptr);
+            std::memcpy(k2.wait_val, ks.wait_val, sizeof k2.wait_val);
+            k2.nwait = ks.nwait;
+          }
+          if (i + 1 == seq.size()) {
+            std::memcpy(k2.sig_ptr, ks.sig_ptr, sizeof k2.sig_ptr);
+            k2.nsig = ks.nsig;
+            k2.sig_val = ks.sig_val;
+            k2.ctr = ks.ctr;
+          }
+          cudaEvent_t a;
+          if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+          if ((rc = run_kernel(ctx, t, q, scalars, k2, seq[i].first))) return rc;
+          if ((rc = timed_end(ctx, g.stream, kernel, a, i == 0 ? 1 : 0))) return rc;
+        }
+        if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+        ctx->pulled_on_comm[q] = 0;
       } else if (kern) {
         cudaEvent_t a;
-        if ((rc = timed_begin(ctx, q, &a))) return rc;
-        if ((rc = run_kernel(ctx, t, q, scalars))) return rc;
-        if ((rc = timed_end(ctx, q, kernel, a))) return rc;
+        if ((rc = timed_begin(ctx, stream_of(ctx, q), &a))) return rc;
+        if ((rc = run_kernel(ctx, t, q, scalars, ks))) return rc;
+        if ((rc = timed_end(ctx, stream_of(ctx, q), kernel, a))) return rc;
+      } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
+        return rc;
       }
-      if (defines && (rc = signal_prod(ctx, q, k))) return rc;
     }
   }
+  for (int q = 0; q < ctx->P && !ctx->plan_only; q++)
+    if (ctx->pulled_on_comm[q]) {
+      Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+      CK(cudaSetDevice(g.ordinal));
+      CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+      ctx->pulled_on_comm[q] = 0;
+    }
   // every rank knows every device's definitions (SPMD replicated tracker)
   for (int q = 0; q < ctx->P; q++)
     for (size_t i = 0; i < ci.arrays.size(); i++)
@@ -752,6 +918,8 @@ static hda_ctx_t* new_ctx(int P) {
   ctx->recv_stage.assign(P, nullptr);
   ctx->send_cap.assign(P, 0);
   ctx->recv_cap.assign(P, 0);
+  ctx->pulled_on_comm.assign(P, 0);
+  ctx->cur_pull.assign(P, nullptr);
   return ctx;
 }
 
@@ -759,6 +927,9 @@ static int setup_gpu_common(hda_ctx_t* ctx) {
   for (auto& g : ctx->gpus) {
     CK(cudaSetDevice(g.ordinal));
     CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g.comm, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g.ev_pull, cudaEventDisableTiming));
   }
   CK(cudaHostAlloc((void**)&ctx->err_host, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
   *ctx->err_host = 0;
@@ -879,6 +1050,9 @@ int hda_finalize(hda_ctx_t* ctx) {
     for (auto& gp : ctx->gpus) {
       cudaSetDevice(gp.ordinal);
       cudaStreamDestroy(gp.stream);
+      cudaStreamDestroy(gp.comm);
+      cudaEventDestroy(gp.ev_fork);
+      cudaEventDestroy(gp.ev_pull);
     }
     if (ctx->err_host) cudaFreeHost(ctx->err_host);
   }
@@ -1123,6 +1297,12 @@ int hda_set_transport(hda_ctx_t* ctx, int32_t transport) {
   return HDA_OK;
 }
 
+int hda_set_overlap(hda_ctx_t* ctx, int32_t enabled) {
+  GUARD();
+  ctx->overlap = enabled != 0;
+  return HDA_OK;
+}
+
 int hda_set_plan_cache(hda_ctx_t* ctx, int32_t enabled) {
   GUARD();
   ctx->cache_on = enabled != 0;
@@ -1145,10 +1325,10 @@ static int drain_timing(hda_ctx_t* ctx) {
     CK(cudaEventElapsedTime(&ms, e.a, e.b));
     if (e.kind == -100) {
       ctx->xtime_ms += ms;
-      ctx->xcount++;
+      ctx->xcount += e.count;
     } else if (e.kind >= 0 && e.kind < KN_COUNT) {
       ctx->ktime_ms[e.kind] += ms;
-      ctx->kcount[e.kind]++;
+      ctx->kcount[e.kind] += e.count;
     }
     ctx->ev_pool.push_back(e.a);
     ctx->ev_pool.push_back(e.b);

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "sync.cuh"
 
 namespace hda {
 
@@ -22,8 +23,19 @@ namespace hda {
 // strided rectangle copy
 // =====================================================================================
 
-int64_t run_desc_units(RunDesc& d) {
+// NVLink pulls are latency-bound unless enough bytes are in flight: aim for >= ~8
+// warps per SM (148 x 8 units), chunks between 512 B and 8 KiB
+int64_t pick_chunk_bytes(int64_t total_bytes) {
+  int64_t c = total_bytes / (148 * 8);
+  c = (c + 511) & ~(int64_t)511;
+  if (c < 512) c = 512;
+  if (c > kChunkBytes) c = kChunkBytes;
+  return c;
+}
+
+int64_t run_desc_units(RunDesc& d, int64_t chunk_bytes) {
   int64_t runs = (int64_t)d.n0 * d.n1;
+  d.chunk_bytes = chunk_bytes;
   if (runs == 0 || d.run_bytes == 0) {
     d.chunks = 1;
     return 0;
@@ -32,7 +44,7 @@ int64_t run_desc_units(RunDesc& d) {
     d.chunks = 0;
     return (runs + 31) / 32;
   }
-  d.chunks = (int32_t)((d.run_bytes + kChunkBytes - 1) / kChunkBytes);
+  d.chunks = (int32_t)((d.run_bytes + chunk_bytes - 1) / chunk_bytes);
   return runs * d.chunks;
 }
 
@@ -69,7 +81,9 @@ __device__ __forceinline__ void warp_copy(char* d, const char* s, int64_t n, int
   }
 }
 
-__global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ RunBatch b) {
+__global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ RunBatch b,
+                                                        const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -83,8 +97,8 @@ __global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ 
       const int64_t i0 = run / d.n1, i1 = run - i0 * d.n1;
       const char* s = d.src + d.src_off + i0 * d.src_p0 + i1 * d.src_p1;
       char* t = d.dst + d.dst_off + i0 * d.dst_p0 + i1 * d.dst_p1;
-      const int64_t b0 = c * kChunkBytes;
-      const int64_t b1 = min(b0 + kChunkBytes, d.run_bytes);
+      const int64_t b0 = c * d.chunk_bytes;
+      const int64_t b1 = min(b0 + d.chunk_bytes, d.run_bytes);
       warp_copy(t + b0, s + b0, b1 - b0, d.es, lane);
     } else {
       const int64_t run = lu * 32 + lane;
@@ -96,13 +110,15 @@ __global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ 
       }
     }
   }
+  ks_post(ks);
 }
 
-cudaError_t launch_copy_runs(const RunBatch& b, cudaStream_t s) {
-  if (b.total_units <= 0) return cudaSuccess;
+cudaError_t launch_copy_runs(const RunBatch& b, const KSync& ks, cudaStream_t s) {
+  if (b.total_units <= 0 && ks.nwait == 0 && ks.nsig == 0) return cudaSuccess;
   int64_t blocks = (b.total_units + 7) / 8;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  copy_runs_kernel<<<(unsigned)blocks, 256, 0, s>>>(b);
+  if (blocks < 1) blocks = 1;
+  copy_runs_kernel<<<(unsigned)blocks, 256, 0, s>>>(b, ks);
   return cudaGetLastError();
 }
 
@@ -224,7 +240,9 @@ __global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST
     stencil2d_kernel(const T* __restrict__ in,
                                                              T* __restrict__ out, int64_t ld,
                                                              int64_t r0, int64_t r1, int64_t c0,
-                                                             int64_t c1, int64_t cbase) {
+                                                             int64_t c1, int64_t cbase,
+                                                             const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   constexpr int V = V16<T>::n;
   constexpr int W = ST_GROUP + 2;
   const int lane = threadIdx.x & 31;
@@ -310,26 +328,31 @@ __global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST
       rgt[1] = rgt[ST_GROUP + 1];
     }
   }
+  ks_post(ks);
 }
 
 // scalar fallback for row pitches that are not 16-byte multiples (small test shapes)
 template <typename T, int KIND>
 __global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
-                                        int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+                                        int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                                        const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = r0 + blockIdx.y;
-  if (c >= c1 || r >= r1) return;
-  const T* p = in + r * ld + c;
-  if (KIND == 0) {
-    out[r * ld + c] = quarter<T>(((p[-1] + p[1]) + p[-ld]) + p[ld]);
-  } else {
-    out[r * ld + c] = st9<T>(p[-1], p[1], p[-ld], p[ld], p[-ld - 1], p[-ld + 1], p[ld - 1], p[ld + 1]);
+  if (c < c1 && r < r1) {
+    const T* p = in + r * ld + c;
+    if (KIND == 0) {
+      out[r * ld + c] = quarter<T>(((p[-1] + p[1]) + p[-ld]) + p[ld]);
+    } else {
+      out[r * ld + c] = st9<T>(p[-1], p[1], p[-ld], p[ld], p[-ld - 1], p[-ld + 1], p[ld - 1], p[ld + 1]);
+    }
   }
+  ks_post(ks);
 }
 
 template <typename T, int KIND>
 static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* lb,
-                                      const int64_t* ub, cudaStream_t s) {
+                                      const int64_t* ub, const KSync& ks, cudaStream_t s) {
   const int64_t ld = shape[2];
   const int64_t r0 = lb[1], r1 = ub[1], c0 = lb[2], c1 = ub[2];
   if (r0 >= r1 || c0 >= c1 || lb[0] >= ub[0]) return cudaSuccess;
@@ -341,26 +364,26 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     const int64_t cbase = c0 - (c0 % V);
     const int64_t per_block = (int64_t)ST_THREADS * V;
     dim3 grid((unsigned)((c1 - cbase + per_block - 1) / per_block), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));
-    stencil2d_kernel<T, KIND, ROWS><<<grid, ST_THREADS, 0, s>>>(in, out, ld, r0, r1, c0, c1, cbase);
+    stencil2d_kernel<T, KIND, ROWS><<<grid, ST_THREADS, 0, s>>>(in, out, ld, r0, r1, c0, c1, cbase, ks);
   } else {
     dim3 grid((unsigned)((c1 - c0 + 127) / 128), (unsigned)(r1 - r0));
-    stencil2d_scalar_kernel<T, KIND><<<grid, 128, 0, s>>>(in, out, ld, r0, r1, c0, c1);
+    stencil2d_scalar_kernel<T, KIND><<<grid, 128, 0, s>>>(in, out, ld, r0, r1, c0, c1, ks);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
-                           const int64_t* ub, cudaStream_t s) {
+                           const int64_t* ub, const KSync& ks, cudaStream_t s) {
   if (dtype == 0)
-    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lb, ub, s);
-  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lb, ub, s);
+    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lb, ub, ks, s);
+  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lb, ub, ks, s);
 }
 
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
-                            const int64_t* ub, cudaStream_t s) {
+                            const int64_t* ub, const KSync& ks, cudaStream_t s) {
   if (dtype == 0)
-    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lb, ub, s);
-  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lb, ub, s);
+    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lb, ub, ks, s);
+  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lb, ub, ks, s);
 }
 
 // =====================================================================================
@@ -373,15 +396,29 @@ constexpr int S3_BY = 8;   // warps per block (rows in y)
 constexpr int S3_ZCH = 16; // planes per block
 
 template <typename T>
+__device__ __forceinline__ void stencil7_rows(const T* __restrict__ in, T* __restrict__ out, int64_t n1, int64_t n2,
+                                              int64_t z0, int64_t z1, int64_t x0, int64_t x1, int64_t x, int64_t y,
+                                              int lane);
+
+template <typename T>
 __global__ void __launch_bounds__(32 * S3_BY) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out,
                                                              int64_t n1, int64_t n2, int64_t z0, int64_t z1,
                                                              int64_t y0, int64_t y1, int64_t x0, int64_t x1,
-                                                             int64_t xbase) {
+                                                             int64_t xbase, const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   constexpr int V = V16<T>::n;
   const int lane = threadIdx.x;
   const int64_t x = xbase + ((int64_t)blockIdx.x * 32 + lane) * V;
   const int64_t y = y0 + (int64_t)blockIdx.y * S3_BY + threadIdx.y;
-  if (y >= y1) return;  // warp-uniform
+  if (y < y1) stencil7_rows<T>(in, out, n1, n2, z0, z1, x0, x1, x, y, lane);  // warp-uniform
+  ks_post(ks);
+}
+
+template <typename T>
+__device__ __forceinline__ void stencil7_rows(const T* __restrict__ in, T* __restrict__ out, int64_t n1, int64_t n2,
+                                              int64_t z0, int64_t z1, int64_t x0, int64_t x1, int64_t x, int64_t y,
+                                              int lane) {
+  constexpr int V = V16<T>::n;
   const bool live = x < n2;
   const int64_t zs = z0 + (int64_t)blockIdx.z * S3_ZCH;
   const int64_t ze = min(zs + (int64_t)S3_ZCH, z1);
@@ -438,24 +475,28 @@ __global__ void __launch_bounds__(32 * S3_BY) stencil7_kernel(const T* __restric
 
 template <typename T>
 __global__ void stencil7_scalar_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n1, int64_t n2,
-                                       int64_t z0, int64_t y0, int64_t y1, int64_t x0, int64_t x1) {
+                                       int64_t z0, int64_t y0, int64_t y1, int64_t x0, int64_t x1,
+                                       const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   const int64_t x = x0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t y = y0 + blockIdx.y;
   const int64_t z = z0 + blockIdx.z;
-  if (x >= x1 || y >= y1) return;
-  const int64_t pl = n1 * n2;
-  const T* p = in + z * pl + y * n2 + x;
-  T s = p[-1] + p[1];
-  s = s + p[-n2];
-  s = s + p[n2];
-  s = s + p[-pl];
-  s = s + p[pl];
-  out[z * pl + y * n2 + x] = s / T(6);
+  if (x < x1 && y < y1) {
+    const int64_t pl = n1 * n2;
+    const T* p = in + z * pl + y * n2 + x;
+    T s = p[-1] + p[1];
+    s = s + p[-n2];
+    s = s + p[n2];
+    s = s + p[-pl];
+    s = s + p[pl];
+    out[z * pl + y * n2 + x] = s / T(6);
+  }
+  ks_post(ks);
 }
 
 template <typename T>
 static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, const int64_t* lb,
-                                     const int64_t* ub, cudaStream_t s) {
+                                     const int64_t* ub, const KSync& ks, cudaStream_t s) {
   const int64_t n1 = shape[1], n2 = shape[2];
   if (lb[0] >= ub[0] || lb[1] >= ub[1] || lb[2] >= ub[2]) return cudaSuccess;
   constexpr int V = V16<T>::n;
@@ -467,18 +508,18 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
     dim3 grid((unsigned)((ub[2] - xbase + per - 1) / per), (unsigned)((ub[1] - lb[1] + S3_BY - 1) / S3_BY),
               (unsigned)((ub[0] - lb[0] + S3_ZCH - 1) / S3_ZCH));
     stencil7_kernel<T><<<grid, dim3(32, S3_BY), 0, s>>>(in, out, n1, n2, lb[0], ub[0], lb[1], ub[1], lb[2],
-                                                       ub[2], xbase);
+                                                       ub[2], xbase, ks);
   } else {
     dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));
-    stencil7_scalar_kernel<T><<<grid, 128, 0, s>>>(in, out, n1, n2, lb[0], lb[1], ub[1], lb[2], ub[2]);
+    stencil7_scalar_kernel<T><<<grid, 128, 0, s>>>(in, out, n1, n2, lb[0], lb[1], ub[1], lb[2], ub[2], ks);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
-                            const int64_t* ub, cudaStream_t s) {
-  if (dtype == 0) return launch_stencil7_t<double>((const double*)in, (double*)out, shape, lb, ub, s);
-  return launch_stencil7_t<float>((const float*)in, (float*)out, shape, lb, ub, s);
+                            const int64_t* ub, const KSync& ks, cudaStream_t s) {
+  if (dtype == 0) return launch_stencil7_t<double>((const double*)in, (double*)out, shape, lb, ub, ks, s);
+  return launch_stencil7_t<float>((const float*)in, (float*)out, shape, lb, ub, ks, s);
 }
 
 // =====================================================================================
@@ -499,7 +540,9 @@ __device__ __forceinline__ __nv_bfloat16 scale1(__nv_bfloat16 x, double a) {
 // one block row per (i0, i1) run of the box; threads stride the contiguous dimension
 template <typename T>
 __global__ void __launch_bounds__(256) scale_kernel(T* x, int64_t n1, int64_t n2, int64_t lb0, int64_t lb1,
-                                                    int64_t lb2, int64_t e1, int64_t e2, int64_t runs, double a) {
+                                                    int64_t lb2, int64_t e1, int64_t e2, int64_t runs, double a,
+                                                    const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   for (int64_t run = blockIdx.y + (int64_t)blockIdx.z * gridDim.y; run < runs;
        run += (int64_t)gridDim.y * gridDim.z) {
     const int64_t i0 = run / e1, i1 = run - i0 * e1;
@@ -507,10 +550,11 @@ __global__ void __launch_bounds__(256) scale_kernel(T* x, int64_t n1, int64_t n2
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < e2; j += (int64_t)gridDim.x * blockDim.x)
       row[j] = scale1<T>(row[j], a);
   }
+  ks_post(ks);
 }
 
 cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb, const int64_t* ub,
-                         double alpha, cudaStream_t s) {
+                         double alpha, const KSync& ks, cudaStream_t s) {
   const int64_t e0 = ub[0] - lb[0], e1 = ub[1] - lb[1], e2 = ub[2] - lb[2];
   if (e0 <= 0 || e1 <= 0 || e2 <= 0) return cudaSuccess;
   const int64_t runs = e0 * e1;
@@ -519,12 +563,12 @@ cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t
   int64_t gz = std::min<int64_t>((runs + gy - 1) / gy, 64);
   dim3 grid(gx, (unsigned)gy, (unsigned)gz);
   if (dtype == 0)
-    scale_kernel<double><<<grid, 256, 0, s>>>((double*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha);
+    scale_kernel<double><<<grid, 256, 0, s>>>((double*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha, ks);
   else if (dtype == 1)
-    scale_kernel<float><<<grid, 256, 0, s>>>((float*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha);
+    scale_kernel<float><<<grid, 256, 0, s>>>((float*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha, ks);
   else
     scale_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>((__nv_bfloat16*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1,
-                                                      e2, runs, alpha);
+                                                      e2, runs, alpha, ks);
   return cudaGetLastError();
 }
 
@@ -536,7 +580,8 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
 }
 
 __global__ void stamp_kernel(char* x, int es, int64_t n1, int64_t n2, const __grid_constant__ BoxList bl,
-                             unsigned long long seed) {
+                             unsigned long long seed, const __grid_constant__ KSync ks) {
+  ks_pre(ks);
   const unsigned long long base = seed * 0x9E3779B97F4A7C15ULL;
   for (int b = 0; b < bl.n; b++) {
     const int64_t e0 = bl.ub[b][0] - bl.lb[b][0], e1 = bl.ub[b][1] - bl.lb[b][1], e2 = bl.ub[b][2] - bl.lb[b][2];
@@ -551,12 +596,13 @@ __global__ void stamp_kernel(char* x, int es, int64_t n1, int64_t n2, const __gr
       else *reinterpret_cast<unsigned short*>(p) = (unsigned short)h;
     }
   }
+  ks_post(ks);
 }
 
 cudaError_t launch_stamp(int es, void* x, const int64_t* shape, const BoxList& boxes, unsigned long long seed,
-                         cudaStream_t s) {
-  if (boxes.n <= 0) return cudaSuccess;
-  stamp_kernel<<<148 * 4, 256, 0, s>>>((char*)x, es, shape[1], shape[2], boxes, seed);
+                         const KSync& ks, cudaStream_t s) {
+  if (boxes.n <= 0 && ks.nwait == 0 && ks.nsig == 0) return cudaSuccess;
+  stamp_kernel<<<148 * 4, 256, 0, s>>>((char*)x, es, shape[1], shape[2], boxes, seed, ks);
   return cudaGetLastError();
 }
 

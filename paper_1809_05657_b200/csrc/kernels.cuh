@@ -23,6 +23,7 @@ struct RunDesc {
   int32_t es;           // element size: granularity of heads/tails/misaligned copies
   int32_t chunks;       // >0: long runs, chunks per run (one warp per chunk)
                         // 0 : short runs, 32 runs per unit (one thread per run)
+  int64_t chunk_bytes;  // bytes per chunk (multiple of 512)
 };
 
 constexpr int kMaxRunDescs = 24;
@@ -33,8 +34,10 @@ struct RunBatch {
 };
 constexpr int64_t kChunkBytes = 8192;
 
-// sets chunks/unit_begin and returns the number of units of one descriptor
-int64_t run_desc_units(RunDesc& d);
+// sets chunks/chunk_bytes and returns the number of units of one descriptor;
+// chunk_bytes adapts so that small payloads still spread over many warps
+int64_t run_desc_units(RunDesc& d, int64_t chunk_bytes);
+int64_t pick_chunk_bytes(int64_t total_bytes);
 
 // cross-device ordering words (see hda.cpp "sync protocol")
 constexpr int kMaxDev = 64;
@@ -49,31 +52,43 @@ struct SignalList {
   unsigned long long val;
 };
 
+// in-kernel cross-device ordering (sync.cuh); nwait == nsig == 0 means "none"
+struct KSync {
+  unsigned long long* wait_ptr[kMaxDev];
+  unsigned long long wait_val[kMaxDev];
+  unsigned long long* sig_ptr[kMaxDev];
+  unsigned long long sig_val;
+  unsigned int* ctr;
+  int* err;
+  long long timeout_ns;
+  int32_t nwait, nsig;
+};
+
 struct BoxList {  // boxes in element coordinates of a 3-D padded shape
   int64_t lb[16][3];
   int64_t ub[16][3];
   int32_t n;
 };
 
-cudaError_t launch_copy_runs(const RunBatch& b, cudaStream_t s);
+cudaError_t launch_copy_runs(const RunBatch& b, const KSync& ks, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, int* err_flag, long long timeout_ns, cudaStream_t s);
 cudaError_t launch_signal(const SignalList& l, cudaStream_t s);
 
 // user kernels over the work box [lb, ub) of one device's replica (padded 3-D shape)
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
-                           const int64_t* lb, const int64_t* ub, cudaStream_t s);
+                           const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape,
-                            const int64_t* lb, const int64_t* ub, cudaStream_t s);
+                            const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape,
-                            const int64_t* lb, const int64_t* ub, cudaStream_t s);
+                            const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb,
-                         const int64_t* ub, double alpha, cudaStream_t s);
+                         const int64_t* ub, double alpha, const KSync& ks, cudaStream_t s);
 cudaError_t launch_stamp(int es, void* x, const int64_t* shape, const BoxList& boxes,
-                         unsigned long long seed, cudaStream_t s);
+                         unsigned long long seed, const KSync& ks, cudaStream_t s);
 // C[rows lb0..ub0, cols lb1..ub1] = alpha * A@B + beta*C ; A [M,K] bf16 row-major,
 // B [K,N] bf16 row-major, C [M,N] f32 or bf16 row-major (full-array strides)
 cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N,
                         int64_t K, const int64_t* lb, const int64_t* ub, float alpha, float beta,
-                        cudaStream_t s);
+                        const KSync& ks, cudaStream_t s);
 
 }  // namespace hda

@@ -1,0 +1,58 @@
+// sync.cuh — cross-device ordering folded into the kernels that need it.
+// ks_pre:  before a kernel touches its data, one thread per CTA spins (with a
+//          timeout) until every listed sync word reaches its epoch (RAW for pulls,
+//          WAR for kernels that overwrite cells peers may still be reading).
+// ks_post: the last CTA to finish (device-scope counter) publishes the call epoch
+//          to the listed words of the peers with system-scope release stores.
+#pragma once
+#include "kernels.cuh"
+
+namespace hda {
+
+__device__ __forceinline__ unsigned long long ks_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ks_st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ks_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void ks_pre(const KSync& s) {
+  if (s.nwait == 0) return;
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x + threadIdx.z * blockDim.x * blockDim.y;
+  if (tid < s.nwait) {
+    const unsigned long long t0 = ks_timer();
+    while (ks_ld_acquire(s.wait_ptr[tid]) < s.wait_val[tid]) {
+      __nanosleep(64);
+      if ((long long)(ks_timer() - t0) > s.timeout_ns) {
+        *reinterpret_cast<volatile int*>(s.err) = -7;
+        __threadfence_system();
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void ks_post(const KSync& s) {
+  if (s.nsig == 0) return;
+  __syncthreads();
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x + threadIdx.z * blockDim.x * blockDim.y;
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(s.ctr, 1u) == total - 1) {
+      *s.ctr = 0;  // stream-ordered reuse by the next kernel of this purpose
+      __threadfence_system();
+      for (int i = 0; i < s.nsig; i++) ks_st_release(s.sig_ptr[i], s.sig_val);
+    }
+  }
+}
+
+}  // namespace hda

@@ -46,7 +46,7 @@ EXPORTS = [
     "hda_init", "hda_init_spmd", "hda_finalize", "hda_num_devices", "hda_is_local", "hda_spmd_export",
     "hda_spmd_import", "hda_create", "hda_create_ext", "hda_free", "hda_device_ptr", "hda_partition",
     "hda_partition_manual", "hda_partition_region", "hda_apply", "hda_sync", "hda_write", "hda_read",
-    "hda_set_transport", "hda_set_plan_cache", "hda_set_kernel_timing", "hda_kernel_time", "hda_exchange_time",
+    "hda_set_transport", "hda_set_overlap", "hda_set_plan_cache", "hda_set_kernel_timing", "hda_kernel_time", "hda_exchange_time",
     "hda_stream", "hda_last_plan", "hda_owner_map", "hda_read_replica", "hda_stats", "hda_reset_stats",
     "hda_last_error", "hda_version",
 ]
@@ -85,6 +85,7 @@ def lib():
             "hda_read": [vp, i32, i32, vp],
             "hda_set_transport": [vp, i32],
             "hda_set_plan_cache": [vp, i32],
+            "hda_set_overlap": [vp, i32],
             "hda_set_kernel_timing": [vp, i32],
             "hda_kernel_time": [vp, i32, P(ctypes.c_double), P(i64)],
             "hda_exchange_time": [vp, P(ctypes.c_double), P(i64)],
@@ -273,6 +274,9 @@ class HDArray:
     # ---- tuning / timing
     def set_transport(self, t):
         self._chk(self.L.hda_set_transport(self.h, t))
+
+    def set_overlap(self, on):
+        self._chk(self.L.hda_set_overlap(self.h, 1 if on else 0))
 
     def set_plan_cache(self, on):
         self._chk(self.L.hda_set_plan_cache(self.h, 1 if on else 0))
