@@ -369,7 +369,7 @@ def main():
     ap.add_argument("--e2e-sweeps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--transport", type=int, default=0)
+    ap.add_argument("--transport", type=int, default=2, help="0 fused SM pull, 1 staged, 2 auto (default)")
     ap.add_argument("--no-overlap", action="store_true")
     args = ap.parse_args()
     defaults = {"jacobi2d": (1000, 20), "stencil9": (200, 10), "stencil7": (100, 5), "repartition": (40, 4),
@@ -561,7 +561,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype_name, "data": "synthetic",
             "config": {"workload": wl.workload, "n": wl.n, "parallelism": f"spmd{ws}" if ws > 1 else "single",
-                       "transport": ["fused", "staged"][args.transport], "overlap": not args.no_overlap,
+                       "transport": ["fused", "staged", "auto"][args.transport], "overlap": not args.no_overlap,
                        "l2": ("L2 flushed between timed steps" if flush else
                               f"inputs larger than L2 (per-GPU working set {wl.working_set / 2**20:.0f} MiB)")},
             "roofline": roof,

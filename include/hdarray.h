@@ -110,8 +110,11 @@ enum hda_kernel {
 enum hda_transport {
   HDA_XPORT_FUSED = 0,   /* one SM kernel on the receiver: peer loads -> local stores
                             (pack + NVLink transfer + unpack fused, no staging) */
-  HDA_XPORT_STAGED = 1   /* pack kernel on the sender into a contiguous staging buffer,
+  HDA_XPORT_STAGED = 1,  /* pack kernel on the sender into a contiguous staging buffer,
                             copy-engine transfer to the receiver, unpack kernel there */
+  HDA_XPORT_AUTO = 2     /* default: messages >= 1 MiB from another GPU are strided
+                            copy-engine peer copies (cudaMemcpy3DAsync, no staging, SMs
+                            stay free for the overlapped compute); smaller ones FUSED */
 };
 
 enum hda_status {

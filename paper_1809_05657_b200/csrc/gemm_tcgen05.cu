@@ -197,6 +197,18 @@ __device__ __forceinline__ void store_chunk<__nv_bfloat16>(__nv_bfloat16* row, i
   }
 }
 
+// Tile order: groups of GROUP_M M-tiles, N-major inside a group, so the ~148 tiles in
+// flight share 16 A tiles and ~9 B tiles (both L2-resident) instead of streaming 148
+// distinct A tiles per wave (measured 30.7 GB of DRAM reads for 1 GiB of operands).
+constexpr int GROUP_M = 16;
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n, int& mt, int& nt) {
+  const int64_t per_group = (int64_t)GROUP_M * tiles_n;
+  const int64_t g = t / per_group, local = t - g * per_group;
+  const int64_t rows = min((int64_t)GROUP_M, tiles_m - g * GROUP_M);
+  mt = (int)(g * GROUP_M + local % rows);
+  nt = (int)(local / rows);
+}
+
 template <typename TC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, TC* C,
@@ -244,7 +256,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int mt = (int)(t % tiles_m), nt = (int)(t / tiles_m);
+        int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, mt, nt);
         const int row0 = (int)(m0 + (int64_t)mt * BM), col0 = (int)(n0 + (int64_t)nt * BN);
         for (int kb = 0; kb < kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -302,7 +315,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     int acc = 0;
     uint32_t aph = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const int mt = (int)(t % tiles_m), nt = (int)(t / tiles_m);
+      int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, mt, nt);
       const int64_t row = m0 + (int64_t)mt * BM + q * 32 + lane;
       const int64_t colb = n0 + (int64_t)nt * BN;
       mbar_wait(&tfull[acc], aph);

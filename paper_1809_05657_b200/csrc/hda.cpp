@@ -41,6 +41,7 @@ namespace {
 
 constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_CTR_PULL = 192, SW_CTR_KERN = 193, SW_WORDS = 256;
 constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
+constexpr int64_t kCeBytes = 1 << 20;         // AUTO: messages >= 1 MiB go to the copy engine
 
 struct Gpu {
   int ordinal = 0;
@@ -79,6 +80,7 @@ struct PullJob {
   // incoming rectangle (run while the pull is in flight) and the rest (after it)
   bool split = false;
   std::vector<Box> interior, dependent;
+  std::vector<cudaMemcpy3DParms> ce;  // AUTO transport: bulk messages on the copy engine
 };
 struct PackJob {
   int src;
@@ -99,6 +101,7 @@ struct RecvJob {
 };
 struct ExecPlan {
   bool staged = false;
+  int transport = HDA_XPORT_FUSED;
   std::vector<PullJob> pulls;
   std::vector<PackJob> packs;
   std::vector<RecvJob> recvs;
@@ -121,7 +124,7 @@ struct hda_ctx {
   std::vector<char*> send_stage, recv_stage;
   std::vector<size_t> send_cap, recv_cap;
   std::unordered_map<uint64_t, ExecPlan> exec;
-  int transport = HDA_XPORT_FUSED;
+  int transport = HDA_XPORT_AUTO;
   bool cache_on = true, ktiming = false, overlap = true;
   std::vector<char> pulled_on_comm;  // [P] this call's pull for device q ran on the comm stream
   std::vector<const PullJob*> cur_pull;
@@ -336,6 +339,7 @@ static int ensure_stage(hda_ctx_t* ctx, std::vector<char*>& v, std::vector<size_
 static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
   const int P = ctx->P;
   ep.staged = ctx->transport == HDA_XPORT_STAGED;
+  ep.transport = ctx->transport;
   if (t->msgs.empty()) return HDA_OK;
   if (!ep.staged) {
     for (int q = 0; q < P; q++) {
@@ -348,16 +352,31 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
         const TArray& a = ctx->tr->array(m.array);
         int64_t S[3];
         front_shape(a.ndim, a.shape, S);
-        RunDesc d = rect_desc(S, front_box(a.ndim, m.box), a.es);
+        const Box fb = front_box(a.ndim, m.box);
+        RunDesc d = rect_desc(S, fb, a.es);
         d.src = ctx->arr[m.array].ptr[m.src];
         d.dst = ctx->arr[m.array].ptr[q];
         if (!d.src || !d.dst) return fail(ctx, HDA_ESTATE, "replica not mapped (SPMD handles missing?)");
-        descs.push_back(d);
+        const int64_t bytes = box_volume(m.box) * (int64_t)a.es;
+        if (ctx->transport == HDA_XPORT_AUTO && bytes >= kCeBytes && !same_stream(ctx, m.src, q)) {
+          // bulk: copy-engine peer copy of the strided box (no SM time, no staging)
+          cudaMemcpy3DParms p;
+          std::memset(&p, 0, sizeof p);
+          p.srcPtr = make_cudaPitchedPtr(const_cast<char*>(d.src), (size_t)S[2] * a.es, (size_t)S[2], (size_t)S[1]);
+          p.dstPtr = make_cudaPitchedPtr(d.dst, (size_t)S[2] * a.es, (size_t)S[2], (size_t)S[1]);
+          p.srcPos = p.dstPos = make_cudaPos((size_t)fb.lb[2] * a.es, (size_t)fb.lb[1], (size_t)fb.lb[0]);
+          p.extent = make_cudaExtent((size_t)(fb.ub[2] - fb.lb[2]) * a.es, (size_t)(fb.ub[1] - fb.lb[1]),
+                                     (size_t)(fb.ub[0] - fb.lb[0]));
+          p.kind = cudaMemcpyDefault;
+          job.ce.push_back(p);
+        } else {
+          descs.push_back(d);
+        }
         if (std::find(job.srcs.begin(), job.srcs.end(), m.src) == job.srcs.end()) job.srcs.push_back(m.src);
         std::pair<int, int> pr(m.array, m.src);
         if (std::find(job.pend.begin(), job.pend.end(), pr) == job.pend.end()) job.pend.push_back(pr);
       }
-      if (descs.empty()) continue;
+      if (descs.empty() && job.ce.empty()) continue;
       batch_descs(descs, job.batches);
       for (int p : job.srcs)
         if (!same_stream(ctx, p, q)) job.cross = true;
@@ -499,7 +518,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
   ExecPlan scratch;
   if (ctx->cache_on) {
     auto it = ctx->exec.find(t->serial);
-    if (it == ctx->exec.end() || it->second.staged != (ctx->transport == HDA_XPORT_STAGED)) {
+    if (it == ctx->exec.end() || it->second.transport != ctx->transport) {
       ExecPlan np;
       int rc = build_exec(ctx, t, np);
       if (rc) return rc;
@@ -538,6 +557,24 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
       cudaEvent_t a;
       if ((rc = timed_begin(ctx, st, &a))) return rc;
       const size_t nb = job.batches.size();
+      if (!job.ce.empty()) {  // copy-engine part: RAW wait kernel, then the copies
+        KSync w = ks_empty(ctx);
+        std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
+        std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
+        w.nwait = pre.nwait;
+        RunBatch empty;
+        std::memset(&empty, 0, sizeof empty);
+        if (w.nwait) {
+          CK(launch_copy_runs(empty, w, st));
+          count_launch(ctx);
+        }
+        pre.nwait = 0;
+        for (const cudaMemcpy3DParms& p : job.ce) CK(cudaMemcpy3DAsync(&p, st));
+        if (nb == 0) {
+          CK(launch_copy_runs(empty, post, st));  // ACK signals after the copies
+          count_launch(ctx);
+        }
+      }
       for (size_t i = 0; i < nb; i++) {
         KSync ks = ks_empty(ctx);
         if (i == 0) {
@@ -1290,7 +1327,8 @@ int hda_read(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, void* host_full) 
 
 int hda_set_transport(hda_ctx_t* ctx, int32_t transport) {
   GUARD();
-  if (transport != HDA_XPORT_FUSED && transport != HDA_XPORT_STAGED) return fail(ctx, HDA_EINVAL, "transport");
+  if (transport != HDA_XPORT_FUSED && transport != HDA_XPORT_STAGED && transport != HDA_XPORT_AUTO)
+    return fail(ctx, HDA_EINVAL, "transport");
   if (transport == HDA_XPORT_STAGED && ctx->spmd && ctx->P > 1)
     return fail(ctx, HDA_EUNSUPPORTED, "staged transport is single-process only");
   ctx->transport = transport;

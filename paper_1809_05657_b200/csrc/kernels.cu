@@ -264,8 +264,10 @@ __global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST
   auto edges = [&](const T(&r)[V], int64_t row, T& L, T& R) {
     L = __shfl_up_sync(0xffffffffu, r[V - 1], 1);
     R = __shfl_down_sync(0xffffffffu, r[0], 1);
-    if (lane == 0 && live) L = __ldg(in + row * ld + col - 1);
-    if (lane == 31 && live) R = __ldg(in + row * ld + col + V);
+    // the neighbour of column 0 / ld-1 is never used (work boxes keep a 1-cell ring),
+    // and loading it would step outside the replica for the first / last row
+    if (lane == 0 && live && col > 0) L = __ldg(in + row * ld + col - 1);
+    if (lane == 31 && live && col + V < ld) R = __ldg(in + row * ld + col + V);
   };
 
   load_row(w[0], rs - 1);
@@ -441,8 +443,8 @@ __device__ __forceinline__ void stencil7_rows(const T* __restrict__ in, T* __res
     T L = __shfl_up_sync(0xffffffffu, zc[V - 1], 1);
     T R = __shfl_down_sync(0xffffffffu, zc[0], 1);
     const T* row = in + z * plane + y * n2 + x;
-    if (lane == 0 && live) L = __ldg(row - 1);
-    if (lane == 31 && live) R = __ldg(row + V);
+    if (lane == 0 && live && x > 0) L = __ldg(row - 1);
+    if (lane == 31 && live && x + V < n2) R = __ldg(row + V);
     T o[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
@@ -537,18 +539,30 @@ __device__ __forceinline__ __nv_bfloat16 scale1(__nv_bfloat16 x, double a) {
   return __float2bfloat16_rn(__fmul_rn((float)a, __bfloat162float(x)));
 }
 
-// one block row per (i0, i1) run of the box; threads stride the contiguous dimension
+// one block per (i0, i1) run of the box (grid-stride over runs); threads stride the
+// contiguous dimension with 16-byte vectors on the aligned body, scalars on head/tail
 template <typename T>
 __global__ void __launch_bounds__(256) scale_kernel(T* x, int64_t n1, int64_t n2, int64_t lb0, int64_t lb1,
                                                     int64_t lb2, int64_t e1, int64_t e2, int64_t runs, double a,
                                                     const __grid_constant__ KSync ks) {
   ks_pre(ks);
-  for (int64_t run = blockIdx.y + (int64_t)blockIdx.z * gridDim.y; run < runs;
-       run += (int64_t)gridDim.y * gridDim.z) {
+  constexpr int V = 16 / sizeof(T);
+  for (int64_t run = blockIdx.x; run < runs; run += gridDim.x) {
     const int64_t i0 = run / e1, i1 = run - i0 * e1;
     T* row = x + ((lb0 + i0) * n1 + (lb1 + i1)) * n2 + lb2;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < e2; j += (int64_t)gridDim.x * blockDim.x)
-      row[j] = scale1<T>(row[j], a);
+    int64_t head = (int64_t)(((16 - ((uintptr_t)row & 15)) & 15) / sizeof(T));
+    if (head > e2) head = e2;
+    const int64_t nv = (e2 - head) / V;
+    if (threadIdx.x < head) row[threadIdx.x] = scale1<T>(row[threadIdx.x], a);
+    uint4* body = reinterpret_cast<uint4*>(row + head);
+    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      uint4 u = body[v];
+      T* e = reinterpret_cast<T*>(&u);
+#pragma unroll
+      for (int t = 0; t < V; t++) e[t] = scale1<T>(e[t], a);
+      body[v] = u;
+    }
+    for (int64_t t = head + nv * V + threadIdx.x; t < e2; t += blockDim.x) row[t] = scale1<T>(row[t], a);
   }
   ks_post(ks);
 }
@@ -558,10 +572,7 @@ cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t
   const int64_t e0 = ub[0] - lb[0], e1 = ub[1] - lb[1], e2 = ub[2] - lb[2];
   if (e0 <= 0 || e1 <= 0 || e2 <= 0) return cudaSuccess;
   const int64_t runs = e0 * e1;
-  unsigned gx = (unsigned)std::min<int64_t>((e2 + 255) / 256, 64);
-  int64_t gy = std::min<int64_t>(runs, 65535);
-  int64_t gz = std::min<int64_t>((runs + gy - 1) / gy, 64);
-  dim3 grid(gx, (unsigned)gy, (unsigned)gz);
+  const unsigned grid = (unsigned)std::min<int64_t>(runs, 148 * 64);
   if (dtype == 0)
     scale_kernel<double><<<grid, 256, 0, s>>>((double*)x, shape[1], shape[2], lb[0], lb[1], lb[2], e1, e2, runs, alpha, ks);
   else if (dtype == 1)

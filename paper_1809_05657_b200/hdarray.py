@@ -18,7 +18,7 @@ STAR = -(2**31)
 F64, F32, BF16, I32, I64 = 0, 1, 2, 3, 4
 ROW, COL, BLOCK = 0, 1, 2
 (K_NONE, K_JACOBI5, K_COPY, K_STENCIL9, K_STENCIL7_3D, K_SCALE, K_GEMM, K_STAMP) = range(8)
-XPORT_FUSED, XPORT_STAGED = 0, 1
+XPORT_FUSED, XPORT_STAGED, XPORT_AUTO = 0, 1, 2
 OK, EINVAL, ERANGE, EOVERLAP, ERACE, ENOMEM, ECUDA, ETIMEOUT, EUNSUPPORTED, ESTATE = (
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
 HANDLE_BYTES = 128

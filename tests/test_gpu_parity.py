@@ -53,7 +53,7 @@ def assert_replicas(h, w, arrs, P):
 
 
 # ------------------------------------------------------------------ config 1
-@pytest.mark.parametrize("transport", [0, 1])
+@pytest.mark.parametrize("transport", [0, 1, 2])
 def test_config1_virtual_devices(H, transport):
     """BASELINE configs[0]: 16x16 fp64 Jacobi, 4 row partitions, +-1 offsets; paper
     2-call form on one GPU with 4 virtual devices."""
@@ -321,7 +321,7 @@ def test_multi_gpu_single_process(H, P):
     """P devices over 2 physical GPUs (NVLink peer pulls + cross-GPU sync words)."""
     shape = (258, 514)
     u0 = synth.uniform(3, shape)
-    for transport in (0, 1):
+    for transport in (0, 1, 2):
         h = H.HDArray(n_gpus=2, n_devices=P)
         h.set_transport(transport)
         w = O.Oracle(P)
@@ -336,3 +336,59 @@ def test_multi_gpu_single_process(H, P):
             be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
         assert_replicas(h, w, [X, Y], P)
         h.close()
+    # bulk repartition: blocks >= 1 MiB take the copy-engine path under AUTO
+    big = (1024, 2048)
+    v = synth.uniform(8, big, "f32")
+    for transport in (0, 2):
+        h = H.HDArray(n_gpus=2, n_devices=P)
+        h.set_transport(transport)
+        w = O.Oracle(P)
+        for be in (h, w):
+            Z = be.create(H.F32, big)
+            rp = be.partition(H.ROW, big)
+            cp = be.partition(H.COL, big)
+            be.write(Z, rp, v)
+            for it in range(3):
+                be.apply(H.K_SCALE, cp, [(Z, [(0, 0)], [(0, 0)])], [2.0])
+                be.apply(H.K_SCALE, rp, [(Z, [(0, 0)], [(0, 0)])], [0.5])
+        assert_replicas(h, w, [Z], P)
+        h.close()
+
+
+# ------------------------------------------------------------------ 2MM
+@pytest.mark.parametrize("kind", ["ROW", "COL"])
+def test_2mm_chain_partition_choice(H, kind):
+    """2MM: D = A x B ; E = C x D, iterated.  ROW moves B once and D every
+    iteration; COL moves A and C once.  Integer bf16 inputs keep every product exact,
+    so E (fp32) is bit-exact vs the oracle; messages equal element by element."""
+    n, P, iters = 256, 4, 3
+    S = H.STAR
+    Ab, Bb, Cb = (synth.int_bf16(60 + i, (n, n), -2, 2) for i in range(3))
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    moved = []
+    for be in (h, w):
+        A = be.create(H.BF16, (n, n))
+        B = be.create(H.BF16, (n, n))
+        C = be.create(H.BF16, (n, n))
+        D = be.create(H.BF16, (n, n))
+        E = be.create(H.F32, (n, n))
+        part = be.partition(getattr(H, kind), (n, n))
+        for X, v in ((A, Ab), (B, Bb), (C, Cb)):
+            be.write(X, part, v)
+    for it in range(iters):
+        for be in (h, w):
+            be.apply(H.K_GEMM, part, [(D, [], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.0, 0.0])
+        assert_same_msgs(h, w)
+        m1 = {k[0] for k in O.msgs_by_pair(w.msgs())}
+        for be in (h, w):
+            be.apply(H.K_GEMM, part, [(E, [], [(0, 0)]), (C, [(0, S)], []), (D, [(S, 0)], [])], [1.0, 0.0])
+        assert_same_msgs(h, w)
+        m2 = {k[0] for k in O.msgs_by_pair(w.msgs())}
+        moved.append((m1, m2))
+    if kind == "ROW":
+        assert moved[0] == ({B}, {D}) and all(m == (set(), {D}) for m in moved[1:])
+    else:
+        assert moved[0] == ({A}, {C}) and all(m == (set(), set()) for m in moved[1:])
+    assert_replicas(h, w, [D, E], P)
+    h.close()

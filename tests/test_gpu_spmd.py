@@ -35,6 +35,7 @@ def _worker(rank, world, port, q):
         import paper_1809_05657_b200 as H
         import synth
         h = H.HDArray.spmd(world, rank, rank)
+        h.set_transport(int(os.environ.get("HDA_TEST_TRANSPORT", "2")))
         w = O.Oracle(world)
         shape = (130, 262)
         u0 = synth.uniform(5, shape)
@@ -63,6 +64,18 @@ def _worker(rank, world, port, q):
             be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
             be.apply(H.K_SCALE, full, [(X, [(0, 0)], [(0, 0)])], [0.5])
         check("repart", [X])
+        # bulk ROW<->COL blocks (>= 1 MiB) through the copy engine under AUTO
+        big = (1024, 2048)
+        v = synth.uniform(8, big, "f32")
+        for be in (h, w):
+            Z = be.create(H.F32, big)
+            rp = be.partition(H.ROW, big)
+            cp = be.partition(H.COL, big)
+            be.write(Z, rp, v)
+            for it in range(3):
+                be.apply(H.K_SCALE, cp, [(Z, [(0, 0)], [(0, 0)])], [2.0])
+                be.apply(H.K_SCALE, rp, [(Z, [(0, 0)], [(0, 0)])], [0.5])
+        check("bulk", [Z])
         got = h.read(X, full)
         ref = w.read(X, full)
         lb, ub = h.region(full, rank, 2)
