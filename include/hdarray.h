@@ -230,6 +230,16 @@ int hda_sync(hda_ctx_t* ctx);
 int hda_write(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, const void* host_full);
 int hda_read(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, void* host_full);
 
+/* Reduce (Table 2 Reduce; "a device reduction is performed
+ * followed by an MPI reduction"): coherence for LUSE_p = region_p (exactly as
+ * hda_read), then a deterministic two-pass reduction of region_p on every device
+ * (fp64 accumulation; int64 for integer dtypes), then the P partials are combined in
+ * device order — over NVLink sync words in SPMD mode, so every rank returns the same
+ * value.  Regions are disjoint, so every cell counts once.  Blocks.
+ * ESTATE on plan-only contexts. */
+enum hda_reduce_op { HDA_SUM = 0, HDA_PROD = 1, HDA_MAX = 2, HDA_MIN = 3 };
+int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, double* out);
+
 /* ---- transport / tuning ---- */
 int hda_set_transport(hda_ctx_t* ctx, int32_t transport);
 /* overlap on/off (default on): when a device's halo comes from another GPU, its pull

@@ -32,6 +32,7 @@ F64, F32, BF16, I32, I64 = 0, 1, 2, 3, 4
 ROW, COL, BLOCK = 0, 1, 2
 K_NONE, K_JACOBI5, K_COPY, K_STENCIL9, K_STENCIL7_3D, K_SCALE, K_GEMM, K_STAMP = range(8)
 OK, EINVAL, ERANGE, EOVERLAP, ERACE, ENOMEM = 0, -1, -2, -3, -4, -5
+SUM, PROD, MAX, MIN = 0, 1, 2, 3
 EUNSUPPORTED, ESTALE = -8, -10
 
 NP_DTYPE = {F64: np.float64, F32: np.float32, BF16: np.uint16, I32: np.int32, I64: np.int64}
@@ -75,6 +76,11 @@ def lib():
                                 i32p, i32p, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int]
         L.orc_write.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.orc_read.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.orc_apply_abs.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, i32p, i32p, i64p,
+                                    i32p, i64p, ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+        L.orc_trapezoid.argtypes = [i64p, i64p, ctypes.c_int]
+        L.orc_reduce.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.POINTER(ctypes.c_double)]
         L.orc_msg_count.restype = ctypes.c_int64
         L.orc_msg_count.argtypes = [ctypes.c_void_p]
         L.orc_msgs.restype = ctypes.c_int64
@@ -191,6 +197,29 @@ class Oracle:
                                           sc.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                           len(scalars)))
 
+    def apply_abs(self, kernel, part, acc, scalars=()):
+        """acc: list of (array, uses, defs); uses/defs: per device a list of boxes
+        ((lb...), (ub...)) (absolute sections, Table 1 use@/def@)."""
+        P = self.P
+        arrays = [a for a, _, _ in acc]
+        n_use, n_def, ub, db = [], [], [], []
+        for a, uses, defs in acc:
+            for q in range(P):
+                n_use.append(len(uses[q]))
+                n_def.append(len(defs[q]))
+                for lb_, ub_ in uses[q]:
+                    ub += list(lb_) + list(ub_)
+                for lb_, ub_ in defs[q]:
+                    db += list(lb_) + list(ub_)
+        a, ap = _i32(arrays)
+        nu, nup = _i32(n_use)
+        nd, ndp = _i32(n_def)
+        u, up = _i64(ub or [0])
+        d, dp = _i64(db or [0])
+        sc = np.ascontiguousarray(list(scalars) or [0.0], dtype=np.float64)
+        return self._chk(self.L.orc_apply_abs(self.h, kernel, part, len(acc), ap, nup, up, ndp, dp,
+                                              sc.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(scalars)))
+
     def write(self, arr, part, host):
         if host is None:  # plan-only worlds carry no data
             return self._chk(self.L.orc_write(self.h, arr, part, None))
@@ -202,6 +231,11 @@ class Oracle:
             out = np.zeros(self.shapes[arr], dtype=NP_DTYPE[self.dtypes[arr]])
         self._chk(self.L.orc_read(self.h, arr, part, out.ctypes.data))
         return out
+
+    def reduce(self, arr, part, op):
+        out = ctypes.c_double()
+        self._chk(self.L.orc_reduce(self.h, arr, part, op, ctypes.byref(out)))
+        return out.value
 
     def msgs(self):
         """(n, 4) int64: (array, src, dst, linear index), sorted."""
@@ -255,6 +289,17 @@ def gemm_sample(A_bits, B_bits, ii, jj, alpha=1.0, beta=0.0, Cin=None):
     L.orc_gemm_sample(A.ctypes.data, B.ctypes.data, C.ctypes.data if C is not None else None,
                       ni, nj, nk, alpha, beta, ip, jp, len(i), out.ctypes.data)
     return out
+
+
+def trapezoid(corners):
+    """per-row boxes ((r, l), (r+1, r_+1)) of a trapezoid with inclusive corners
+    [(top, ul), (top, ur), (bottom, bl), (bottom, br)]."""
+    L = lib()
+    k, kp = _i64([x for c in corners for x in c])
+    n = L.orc_trapezoid(kp, None, 0)
+    out = np.zeros(max(4 * n, 4), np.int64)
+    L.orc_trapezoid(kp, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n)
+    return [((int(out[4 * i]), int(out[4 * i + 1])), (int(out[4 * i + 2]), int(out[4 * i + 3]))) for i in range(n)]
 
 
 def splitmix64(x: int) -> int:

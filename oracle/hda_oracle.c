@@ -289,8 +289,9 @@ int orc_partition_manual(orc_t* w, int ndim, const int64_t* domain, const int64_
         for (int64_t l = p.lb[d][2]; l < p.ub[d][2]; l++) {
           int64_t c = (i * p.domain[1] + j) * p.domain[2] + l;
           if (who[c] >= 0) {
+            int other = who[c];
             free(who);
-            return fail(w, ORC_EOVERLAP, "devices %d and %d overlap", who[c], d);
+            return fail(w, ORC_EOVERLAP, "devices %d and %d overlap", other, d);
           }
           who[c] = (int8_t)d;
         }
@@ -754,11 +755,12 @@ int orc_apply(orc_t* w, int kernel, int part, int n_acc, const int32_t* arrays,
       for (int64_t c = 0; c < n; c++) {
         if (!m[c]) continue;
         if (definer[c] >= 0 && definer[c] != d) {
+          int other = definer[c];
           free(definer);
           free(m);
           for (int x = 0; x < n_acc; x++) free(defmask[x]);
           free(defmask);
-          return fail(w, ORC_ERACE, "devices %d and %d define the same cell", definer[c], d);
+          return fail(w, ORC_ERACE, "devices %d and %d define the same cell", other, d);
         }
         definer[c] = (int8_t)d;
       }
@@ -840,6 +842,149 @@ int orc_apply(orc_t* w, int kernel, int part, int n_acc, const int32_t* arrays,
   return rc;
 }
 
+/* ---------------- absolute sections + trapezoids ---------------- */
+
+static int64_t floordiv(int64_t a, int64_t b) { /* b > 0 */
+  int64_t q = a / b;
+  if ((a % b) != 0 && a < 0) q--;
+  return q;
+}
+
+int orc_trapezoid(const int64_t* k, int64_t* boxes, int cap) {
+  const int64_t top = k[0], ul = k[1], ur = k[3], bottom = k[4], bl = k[5], br = k[7];
+  const int64_t h = bottom - top;
+  int n = 0;
+  for (int64_t r = top; r <= bottom; r++) {
+    int64_t left = ul, right = ur;
+    if (h > 0) {
+      left = ul + floordiv((r - top) * (bl - ul) * 2 + h, 2 * h);
+      right = ur + floordiv((r - top) * (br - ur) * 2 + h, 2 * h);
+    }
+    if (left > right) continue;
+    if (n < cap) {
+      boxes[4 * n + 0] = r;
+      boxes[4 * n + 1] = left;
+      boxes[4 * n + 2] = r + 1;
+      boxes[4 * n + 3] = right + 1;
+    }
+    n++;
+  }
+  return n;
+}
+
+/* mark the cells of explicit boxes (clipped rejected: out of bounds is ERANGE) */
+static int mark_boxes(orc_t* w, const oarr* a, const int64_t* bx, int nb, unsigned char* mask) {
+  int nd = a->ndim;
+  for (int b = 0; b < nb; b++) {
+    int64_t lo[3] = {0, 0, 0}, hi[3] = {1, 1, 1};
+    for (int k = 0; k < nd; k++) {
+      lo[k] = bx[b * 2 * nd + k];
+      hi[k] = bx[b * 2 * nd + nd + k];
+      if (lo[k] < 0 || hi[k] > a->shape[k] || lo[k] > hi[k]) return fail(w, ORC_ERANGE, "absolute box outside");
+    }
+    for (int64_t i = lo[0]; i < hi[0]; i++)
+      for (int64_t j = lo[1]; j < hi[1]; j++)
+        for (int64_t l = lo[2]; l < hi[2]; l++) mask[lin(a, i, j, l)] = 1;
+  }
+  return ORC_OK;
+}
+
+int orc_apply_abs(orc_t* w, int kernel, int part, int n_acc, const int32_t* arrays, const int32_t* n_use,
+                  const int64_t* uses, const int32_t* n_def, const int64_t* defs, const double* scalars,
+                  int n_scalars) {
+  w->n_msgs = 0;
+  if (kernel != ORC_K_NONE && kernel != ORC_K_STAMP) return fail(w, ORC_EINVAL, "absolute sections: NONE/STAMP");
+  if (part < 0 || part >= w->n_parts) return fail(w, ORC_EINVAL, "partition");
+  if (n_acc < 1 || n_acc > 16) return fail(w, ORC_EINVAL, "n_acc");
+  if (kernel == ORC_K_STAMP && n_scalars < 1) return fail(w, ORC_EINVAL, "STAMP needs seed");
+  const int P = w->P;
+  oarr* A[16];
+  const int64_t* ub_[16][MAXP];
+  const int64_t* db_[16][MAXP];
+  {
+    int64_t uo = 0, dof = 0;
+    for (int e = 0; e < n_acc; e++) {
+      if (arrays[e] < 0 || arrays[e] >= w->n_arrays || !w->arrays[arrays[e]].alive)
+        return fail(w, ORC_EINVAL, "unknown array");
+      A[e] = &w->arrays[arrays[e]];
+      if (kernel == ORC_K_STAMP && e > 0)
+        for (int q = 0; q < P; q++)
+          if (n_def[e * P + q]) return fail(w, ORC_EINVAL, "STAMP defines only param 0");
+      for (int q = 0; q < P; q++) {
+        ub_[e][q] = uses + uo;
+        db_[e][q] = defs + dof;
+        uo += (int64_t)n_use[e * P + q] * 2 * A[e]->ndim;
+        dof += (int64_t)n_def[e * P + q] * 2 * A[e]->ndim;
+      }
+    }
+  }
+  /* definer maps + race check */
+  int8_t* definer[16] = {0};
+  int rc = ORC_OK;
+  unsigned char* m = NULL;
+  for (int e = 0; e < n_acc && rc == ORC_OK; e++) {
+    int any = 0;
+    for (int q = 0; q < P; q++) any |= n_def[e * P + q] > 0;
+    if (!any) continue;
+    definer[e] = (int8_t*)malloc((size_t)A[e]->n);
+    memset(definer[e], -1, (size_t)A[e]->n);
+    m = (unsigned char*)realloc(m, (size_t)A[e]->n);
+    for (int q = 0; q < P && rc == ORC_OK; q++) {
+      memset(m, 0, (size_t)A[e]->n);
+      rc = mark_boxes(w, A[e], db_[e][q], n_def[e * P + q], m);
+      for (int64_t c = 0; c < A[e]->n && rc == ORC_OK; c++) {
+        if (!m[c]) continue;
+        if (definer[e][c] >= 0 && definer[e][c] != q)
+          rc = fail(w, ORC_ERACE, "devices %d and %d define the same cell", definer[e][c], q);
+        definer[e][c] = (int8_t)q;
+      }
+    }
+  }
+  /* validate use boxes before any state change */
+  for (int e = 0; e < n_acc && rc == ORC_OK; e++) {
+    unsigned char* u = (unsigned char*)calloc((size_t)A[e]->n, 1);
+    for (int q = 0; q < P && rc == ORC_OK; q++) rc = mark_boxes(w, A[e], ub_[e][q], n_use[e * P + q], u);
+    free(u);
+  }
+  /* messages + exchange (as in orc_apply) */
+  for (int e = 0; e < n_acc && rc == ORC_OK; e++) {
+    int first = 1;
+    for (int f = 0; f < e; f++)
+      if (arrays[f] == arrays[e]) first = 0;
+    if (!first) continue;
+    unsigned char* need = (unsigned char*)malloc((size_t)A[e]->n);
+    for (int q = 0; q < P && rc == ORC_OK; q++) {
+      memset(need, 0, (size_t)A[e]->n);
+      for (int f = e; f < n_acc; f++)
+        if (arrays[f] == arrays[e]) mark_boxes(w, A[e], ub_[f][q], n_use[f * P + q], need);
+      rc = exchange_for(w, arrays[e], q, need);
+    }
+    free(need);
+  }
+  if (rc == ORC_OK && w->with_data && kernel == ORC_K_STAMP && definer[0]) {
+    for (int q = 0; q < P; q++) {
+      kctx k = {w, q, 0};
+      unsigned char* dm = (unsigned char*)calloc((size_t)A[0]->n, 1);
+      for (int64_t c = 0; c < A[0]->n; c++) dm[c] = definer[0][c] == q;
+      k_stamp(&k, A[0], (uint64_t)scalars[0], dm);
+      free(dm);
+    }
+  }
+  if (rc == ORC_OK)
+    for (int e = 0; e < n_acc; e++) {
+      if (!definer[e]) continue;
+      for (int64_t c = 0; c < A[e]->n; c++)
+        if (definer[e][c] >= 0) {
+          A[e]->owner[c] = definer[e][c];
+          A[e]->valid[c] = 1ULL << definer[e][c];
+        }
+    }
+  for (int e = 0; e < n_acc; e++) free(definer[e]);
+  free(m);
+  if (w->n_msgs > 1) qsort(w->msgs, (size_t)w->n_msgs, 4 * sizeof(int64_t), cmp_quad);
+  return rc;
+}
+
 /* ---------------- Write / Read (Table 2) ---------------- */
 
 /* Write: device p copies region_p from the user array; a definition by p (R8) */
@@ -898,6 +1043,82 @@ int orc_read(orc_t* w, int arr, int part, void* host) {
   free(need);
   if (w->n_msgs > 1) qsort(w->msgs, (size_t)w->n_msgs, 4 * sizeof(int64_t), cmp_quad);
   return rc;
+}
+
+/* ---------------- Reduce (Table 2) ---------------- */
+
+static double cell_value(const oarr* a, int dev, int64_t c) {
+  const unsigned char* p = a->rep[dev] + (size_t)c * a->es;
+  switch (a->dtype) {
+    case ORC_F64: {
+      double v;
+      memcpy(&v, p, 8);
+      return v;
+    }
+    case ORC_F32: {
+      float v;
+      memcpy(&v, p, 4);
+      return (double)v;
+    }
+    case ORC_BF16: {
+      uint16_t v;
+      memcpy(&v, p, 2);
+      return (double)bf16_to_f32(v);
+    }
+    case ORC_I32: {
+      int32_t v;
+      memcpy(&v, p, 4);
+      return (double)v;
+    }
+    default: {
+      int64_t v;
+      memcpy(&v, p, 8);
+      return (double)v;
+    }
+  }
+}
+
+int orc_reduce(orc_t* w, int arr, int part, int op, double* out) {
+  if (op < 0 || op > 3) return fail(w, ORC_EINVAL, "op");
+  if (!w->with_data) return fail(w, ORC_EINVAL, "reduce needs data");
+  int rc = orc_read(w, arr, part, NULL); /* coherence, exactly as a read */
+  if (rc) return rc;
+  const oarr* a = &w->arrays[arr];
+  const opart* pt = &w->parts[part];
+  int is_int = a->dtype == ORC_I32 || a->dtype == ORC_I64;
+  double acc = op == ORC_SUM ? 0.0 : op == ORC_PROD ? 1.0 : op == ORC_MAX ? -INFINITY : INFINITY;
+  int64_t iacc = op == ORC_PROD ? 1 : 0;
+  int first = 1;
+  for (int d = 0; d < w->P; d++) {
+    if (box_empty(pt->lb[d], pt->ub[d])) continue;
+    for (int64_t i = pt->lb[d][0]; i < pt->ub[d][0]; i++)
+      for (int64_t j = pt->lb[d][1]; j < pt->ub[d][1]; j++)
+        for (int64_t l = pt->lb[d][2]; l < pt->ub[d][2]; l++) {
+          int64_t c = lin(a, i, j, l);
+          if (is_int) {
+            int64_t v;
+            if (a->dtype == ORC_I32) {
+              int32_t t;
+              memcpy(&t, a->rep[d] + (size_t)c * 4, 4);
+              v = t;
+            } else {
+              memcpy(&v, a->rep[d] + (size_t)c * 8, 8);
+            }
+            if (op == ORC_SUM) iacc += v;
+            else if (op == ORC_PROD) iacc *= v;
+            else if (first || (op == ORC_MAX ? v > iacc : v < iacc)) iacc = v;
+          } else {
+            double v = cell_value(a, d, c);
+            if (op == ORC_SUM) acc = acc + v;
+            else if (op == ORC_PROD) acc = acc * v;
+            else if (op == ORC_MAX) acc = v > acc ? v : acc;
+            else acc = v < acc ? v : acc;
+          }
+          first = 0;
+        }
+  }
+  *out = is_int ? (double)iacc : acc;
+  return ORC_OK;
 }
 
 /* ---------------- introspection ---------------- */

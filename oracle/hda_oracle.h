@@ -79,8 +79,31 @@ int orc_region(const orc_t* w, int part, int dev, int64_t* lb, int64_t* ub);
 int orc_apply(orc_t* w, int kernel, int part, int n_acc, const int32_t* arrays,
               const int32_t* n_use, const int32_t* uses, const int32_t* n_def,
               const int32_t* defs, const double* scalars, int n_scalars);
-int orc_write(orc_t* w, int arr, int part, const void* host);
+/* absolute sections (Table 1 use@/def@, Table 2 SetAbsoluteUse/Def, P:L171-173,
+ * P:L188-191): entry e of device q uses/defines exactly the listed boxes
+ * (half-open, ndim lb then ndim ub per box), instead of offset compositions.
+ * n_use/n_def are [n_acc*P] box counts (entry-major), boxes concatenated in the same
+ * order.  Kernels: NONE or STAMP. */
+int orc_apply_abs(orc_t* w, int kernel, int part, int n_acc, const int32_t* arrays,
+                  const int32_t* n_use, const int64_t* uses, const int32_t* n_def,
+                  const int64_t* defs, const double* scalars, int n_scalars);
+/* Trapezoid (Table 2 SetTrapezoidUse/Def): inclusive corners
+ * (row,col) upper-left, upper-right, below-left, below-right; upper and lower rows
+ * equal pairwise.  Row r of [top, bottom] spans columns [left(r), right(r)] with
+ * left/right linearly interpolated and rounded half up: left(r) = ul_c +
+ * floor(((r-top)*(bl_c-ul_c)*2 + h) / (2h)), h = bottom-top (h = 0: the top row).
+ * Writes one box per row (rows with left > right are skipped); returns the count. */
+int orc_trapezoid(const int64_t* corners, int64_t* boxes, int cap);
 int orc_read(orc_t* w, int arr, int part, void* host);
+/* Reduce (Table 2; "a device reduction is performed followed by an
+ * MPI reduction"): coherence for LUSE_p = region_p, then every cell of every region,
+ * device 0 first, row-major, folded sequentially in fp64 (int64 for integer dtypes,
+ * returned as double).  op: 0 SUM, 1 PROD, 2 MAX, 3 MIN. */
+#define ORC_SUM 0
+#define ORC_PROD 1
+#define ORC_MAX 2
+#define ORC_MIN 3
+int orc_reduce(orc_t* w, int arr, int part, int op, double* out);
 
 /* messages of the last apply/read as (array, src, dst, linear index) quadruples,
  * sorted by (array, src, dst, index). */

@@ -24,6 +24,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -39,7 +41,10 @@ using namespace hda;
 
 namespace {
 
-constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_CTR_PULL = 192, SW_CTR_KERN = 193, SW_WORDS = 256;
+constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_CTR_PULL = 192, SW_CTR_KERN = 193;
+constexpr int SW_RED = 256, SW_REDSIG = 320;  // reduce partials [P] and their epochs [P]
+constexpr int SW_SCRATCH = 384;               // kReduceBlocks partials
+constexpr int SW_WORDS = SW_SCRATCH + kReduceBlocks;
 constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
 constexpr int64_t kCeBytes = 1 << 20;         // AUTO: messages >= 1 MiB go to the copy engine
 
@@ -1323,6 +1328,70 @@ int hda_read(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, void* host_full) 
   static const int32_t zero[3] = {0, 0, 0};
   AccessIn in{arr, 1, zero, 0, nullptr};
   return call(ctx, KN_READ, part, &in, 1, nullptr, 0, nullptr, host_full);
+}
+
+int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, double* out) {
+  GUARD();
+  if (!out || op < HDA_SUM || op > HDA_MIN) return fail(ctx, HDA_EINVAL, "bad reduce argument");
+  if (!ctx->tr->array_ok(arr)) return fail(ctx, HDA_EINVAL, "unknown array");
+  static const int32_t zero[3] = {0, 0, 0};
+  AccessIn in{arr, 1, zero, 0, nullptr};
+  int rc = call(ctx, KN_READ, part, &in, 1, nullptr, 0, nullptr, nullptr);  // coherence
+  if (rc) return rc;
+  if (ctx->plan_only) return fail(ctx, HDA_ESTATE, "reduce needs data (plan-only context)");
+  const TArray& a = ctx->tr->array(arr);
+  const TPart& pt = ctx->tr->part(part);
+  const bool is_int = a.dtype == DT_I32 || a.dtype == DT_I64;
+  const unsigned long long k = ++ctx->epoch;
+  DevGuard g(true);
+  int64_t S[3];
+  front_shape(a.ndim, a.shape, S);
+  for (int q = 0; q < ctx->P; q++) {
+    if (!ctx->dev[q].local) continue;
+    CK(cudaSetDevice(ordinal_of(ctx, q)));
+    unsigned long long* sw = ctx->dev[q].sync;
+    const Box fb = front_box(a.ndim, pt.box[q]);
+    CK(launch_reduce(a.dtype, ctx->arr[arr].ptr[q], S, fb.lb, fb.ub, op, sw + SW_SCRATCH, sw + SW_RED + q,
+                     stream_of(ctx, q)));
+    count_launch(ctx, 2);
+    if (ctx->spmd && ctx->P > 1) {  // publish this rank's partial to every peer
+      SignalList slots, flags;
+      slots.n = flags.n = 0;
+      flags.val = k;
+      for (int r = 0; r < ctx->P; r++) {
+        if (r == q) continue;
+        slots.ptr[slots.n++] = ctx->dev[r].sync + SW_RED + q;
+        flags.ptr[flags.n++] = ctx->dev[r].sync + SW_REDSIG + q;
+      }
+      CK(launch_share(sw + SW_RED + q, slots, flags, stream_of(ctx, q)));
+      KSync w = ks_empty(ctx);
+      for (int r = 0; r < ctx->P; r++)
+        if (r != q) ks_wait(w, sw + SW_REDSIG + r, k);
+      if ((rc = sync_only(ctx, q, w))) return rc;
+      count_launch(ctx);
+    }
+  }
+  if ((rc = sync_all(ctx))) return rc;
+  // combine the P partials in device order (identical on every rank)
+  double acc = op == HDA_SUM ? 0.0 : op == HDA_PROD ? 1.0 : op == HDA_MAX ? -HUGE_VAL : HUGE_VAL;
+  long long iacc = op == HDA_PROD ? 1 : op == HDA_MAX ? LLONG_MIN : op == HDA_MIN ? LLONG_MAX : 0;
+  for (int p = 0; p < ctx->P; p++) {
+    int src = ctx->spmd ? ctx->rank : p;  // where p's partial lives in this process
+    unsigned long long bits = 0;
+    CK(cudaSetDevice(ordinal_of(ctx, src)));
+    CK(cudaMemcpy(&bits, ctx->dev[src].sync + SW_RED + p, 8, cudaMemcpyDeviceToHost));
+    if (is_int) {
+      long long v;
+      std::memcpy(&v, &bits, 8);
+      iacc = op == HDA_SUM ? iacc + v : op == HDA_PROD ? iacc * v : op == HDA_MAX ? std::max(iacc, v) : std::min(iacc, v);
+    } else {
+      double v;
+      std::memcpy(&v, &bits, 8);
+      acc = op == HDA_SUM ? acc + v : op == HDA_PROD ? acc * v : op == HDA_MAX ? (v > acc ? v : acc) : (v < acc ? v : acc);
+    }
+  }
+  *out = is_int ? (double)iacc : acc;
+  return HDA_OK;
 }
 
 int hda_set_transport(hda_ctx_t* ctx, int32_t transport) {

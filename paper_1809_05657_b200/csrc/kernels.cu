@@ -583,6 +583,138 @@ cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t
   return cudaGetLastError();
 }
 
+// =====================================================================================
+// Reduce (Table 2): fixed-order two-pass reduction -> deterministic
+// =====================================================================================
+template <typename T>
+struct RedIn;
+template <>
+struct RedIn<double> {
+  using A = double;
+  __device__ static A get(double v) { return v; }
+};
+template <>
+struct RedIn<float> {
+  using A = double;
+  __device__ static A get(float v) { return (double)v; }
+};
+template <>
+struct RedIn<__nv_bfloat16> {
+  using A = double;
+  __device__ static A get(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+};
+template <>
+struct RedIn<int> {
+  using A = long long;
+  __device__ static A get(int v) { return (long long)v; }
+};
+template <>
+struct RedIn<long long> {
+  using A = long long;
+  __device__ static A get(long long v) { return v; }
+};
+
+template <typename A>
+__device__ __forceinline__ A red_id(int op) {
+  if (op == 0) return A(0);
+  if (op == 1) return A(1);
+  if (op == 2) return sizeof(A) == 8 && A(0.5) != A(0) ? A(-__longlong_as_double(0x7FF0000000000000LL)) : A(0);
+  return A(0);
+}
+template <>
+__device__ __forceinline__ long long red_id<long long>(int op) {
+  return op == 0 ? 0LL : op == 1 ? 1LL : op == 2 ? (long long)0x8000000000000000ULL : 0x7FFFFFFFFFFFFFFFLL;
+}
+template <>
+__device__ __forceinline__ double red_id<double>(int op) {
+  return op == 0 ? 0.0 : op == 1 ? 1.0 : op == 2 ? -__longlong_as_double(0x7FF0000000000000LL)
+                                                  : __longlong_as_double(0x7FF0000000000000LL);
+}
+template <typename A>
+__device__ __forceinline__ A red_op(int op, A a, A b) {
+  if (op == 0) return a + b;
+  if (op == 1) return a * b;
+  if (op == 2) return b > a ? b : a;
+  return b < a ? b : a;
+}
+
+template <typename A>
+__device__ __forceinline__ A block_tree(A v, int op, A* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = red_op<A>(op, sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) reduce_box_kernel(const T* x, int64_t n1, int64_t n2, int64_t lb0, int64_t lb1,
+                                                         int64_t lb2, int64_t e1, int64_t e2, int64_t runs, int op,
+                                                         typename RedIn<T>::A* partial) {
+  using A = typename RedIn<T>::A;
+  __shared__ A sh[256];
+  A acc = red_id<A>(op);
+  for (int64_t run = blockIdx.x; run < runs; run += gridDim.x) {
+    const int64_t i0 = run / e1, i1 = run - i0 * e1;
+    const T* row = x + ((lb0 + i0) * n1 + (lb1 + i1)) * n2 + lb2;
+    for (int64_t e = threadIdx.x; e < e2; e += blockDim.x) acc = red_op<A>(op, acc, RedIn<T>::get(row[e]));
+  }
+  A r = block_tree<A>(acc, op, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = r;
+}
+
+template <typename A>
+__global__ void __launch_bounds__(256) reduce_final_kernel(const A* partial, int n, int op, A* out) {
+  __shared__ A sh[256];
+  A acc = red_id<A>(op);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = red_op<A>(op, acc, partial[i]);
+  A r = block_tree<A>(acc, op, sh);
+  if (threadIdx.x == 0) *out = r;
+}
+
+template <typename T>
+static cudaError_t reduce_t(const T* x, const int64_t* shape, const int64_t* lb, const int64_t* ub, int op,
+                            void* scratch, void* result, cudaStream_t s) {
+  using A = typename RedIn<T>::A;
+  const int64_t e0 = ub[0] - lb[0], e1 = ub[1] - lb[1], e2 = ub[2] - lb[2];
+  const int64_t runs = (e0 > 0 && e1 > 0 && e2 > 0) ? e0 * e1 : 0;
+  reduce_box_kernel<T><<<kReduceBlocks, 256, 0, s>>>(x, shape[1], shape[2], lb[0], lb[1], lb[2], e1 > 0 ? e1 : 1,
+                                                      e2, runs, op, (A*)scratch);
+  reduce_final_kernel<A><<<1, 256, 0, s>>>((const A*)scratch, kReduceBlocks, op, (A*)result);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce(int dtype, const void* x, const int64_t* shape, const int64_t* lb, const int64_t* ub,
+                          int op, void* scratch, void* result, cudaStream_t s) {
+  switch (dtype) {
+    case 0: return reduce_t<double>((const double*)x, shape, lb, ub, op, scratch, result, s);
+    case 1: return reduce_t<float>((const float*)x, shape, lb, ub, op, scratch, result, s);
+    case 2: return reduce_t<__nv_bfloat16>((const __nv_bfloat16*)x, shape, lb, ub, op, scratch, result, s);
+    case 3: return reduce_t<int>((const int*)x, shape, lb, ub, op, scratch, result, s);
+    default: return reduce_t<long long>((const long long*)x, shape, lb, ub, op, scratch, result, s);
+  }
+}
+
+__global__ void share_kernel(const unsigned long long* local, const __grid_constant__ SignalList slots,
+                             const __grid_constant__ SignalList flags) {
+  const int i = threadIdx.x;
+  const unsigned long long v = *local;
+  if (i < slots.n) {
+    slots.ptr[i][0] = v;
+    __threadfence_system();
+    ks_st_release(flags.ptr[i], flags.val);
+  }
+}
+
+cudaError_t launch_share(const unsigned long long* local, const SignalList& slots, const SignalList& flags,
+                         cudaStream_t s) {
+  if (slots.n <= 0) return cudaSuccess;
+  share_kernel<<<1, kMaxDev, 0, s>>>(local, slots, flags);
+  return cudaGetLastError();
+}
+
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
   unsigned long long z = x + 0x9E3779B97F4A7C15ULL;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;

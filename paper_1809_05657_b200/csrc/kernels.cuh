@@ -85,6 +85,15 @@ cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t
                          const int64_t* ub, double alpha, const KSync& ks, cudaStream_t s);
 cudaError_t launch_stamp(int es, void* x, const int64_t* shape, const BoxList& boxes,
                          unsigned long long seed, const KSync& ks, cudaStream_t s);
+// Reduce: deterministic two-pass reduction of a box (fp64 accumulation, int64 for
+// integer dtypes) into *result (8 bytes); op 0 SUM 1 PROD 2 MAX 3 MIN.  `scratch` holds
+// kReduceBlocks partials.
+constexpr int kReduceBlocks = 592;
+cudaError_t launch_reduce(int dtype, const void* x, const int64_t* shape, const int64_t* lb, const int64_t* ub,
+                          int op, void* scratch, void* result, cudaStream_t s);
+// SPMD combine: copy *local (8 bytes) to every peer slot, then release `val` to their flags
+cudaError_t launch_share(const unsigned long long* local, const SignalList& slots, const SignalList& flags,
+                         cudaStream_t s);
 // C[rows lb0..ub0, cols lb1..ub1] = alpha * A@B + beta*C ; A [M,K] bf16 row-major,
 // B [K,N] bf16 row-major, C [M,N] f32 or bf16 row-major (full-array strides)
 cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N,

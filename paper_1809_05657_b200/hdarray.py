@@ -19,6 +19,7 @@ F64, F32, BF16, I32, I64 = 0, 1, 2, 3, 4
 ROW, COL, BLOCK = 0, 1, 2
 (K_NONE, K_JACOBI5, K_COPY, K_STENCIL9, K_STENCIL7_3D, K_SCALE, K_GEMM, K_STAMP) = range(8)
 XPORT_FUSED, XPORT_STAGED, XPORT_AUTO = 0, 1, 2
+SUM, PROD, MAX, MIN = 0, 1, 2, 3
 OK, EINVAL, ERANGE, EOVERLAP, ERACE, ENOMEM, ECUDA, ETIMEOUT, EUNSUPPORTED, ESTATE = (
     0, -1, -2, -3, -4, -5, -6, -7, -8, -9)
 HANDLE_BYTES = 128
@@ -45,7 +46,7 @@ class hda_stats_t(ctypes.Structure):
 EXPORTS = [
     "hda_init", "hda_init_spmd", "hda_finalize", "hda_num_devices", "hda_is_local", "hda_spmd_export",
     "hda_spmd_import", "hda_create", "hda_create_ext", "hda_free", "hda_device_ptr", "hda_partition",
-    "hda_partition_manual", "hda_partition_region", "hda_apply", "hda_sync", "hda_write", "hda_read",
+    "hda_partition_manual", "hda_partition_region", "hda_apply", "hda_sync", "hda_write", "hda_read", "hda_reduce",
     "hda_set_transport", "hda_set_overlap", "hda_set_plan_cache", "hda_set_kernel_timing", "hda_kernel_time", "hda_exchange_time",
     "hda_stream", "hda_last_plan", "hda_owner_map", "hda_read_replica", "hda_stats", "hda_reset_stats",
     "hda_last_error", "hda_version",
@@ -83,6 +84,7 @@ def lib():
             "hda_sync": [vp],
             "hda_write": [vp, i32, i32, vp],
             "hda_read": [vp, i32, i32, vp],
+            "hda_reduce": [vp, i32, i32, i32, P(ctypes.c_double)],
             "hda_set_transport": [vp, i32],
             "hda_set_plan_cache": [vp, i32],
             "hda_set_overlap": [vp, i32],
@@ -267,6 +269,11 @@ class HDArray:
             out = np.zeros(self.shapes[a], dtype=NP_DTYPE[self.dtypes[a]])
         self._chk(self.L.hda_read(self.h, a, part, out.ctypes.data))
         return out
+
+    def reduce(self, a, part, op):
+        out = ctypes.c_double()
+        self._chk(self.L.hda_reduce(self.h, a, part, op, ctypes.byref(out)))
+        return out.value
 
     def read_ptr(self, a, part, host_ptr: int):
         self._chk(self.L.hda_read(self.h, a, part, ctypes.c_void_p(host_ptr)))

@@ -392,3 +392,41 @@ def test_2mm_chain_partition_choice(H, kind):
         assert moved[0] == ({A}, {C}) and all(m == (set(), set()) for m in moved[1:])
     assert_replicas(h, w, [D, E], P)
     h.close()
+
+
+# ------------------------------------------------------------------ Reduce (§8(f)-3)
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16", "i64"])
+def test_reduce_vs_oracle(H, dtype):
+    """Table 2 Reduce: same coherence messages as a read, then a
+    device reduction + combine.  Integer-valued data: SUM/MAX/MIN exact; random data:
+    SUM within 1e-12 of the sequential fp64 oracle relative to sum|x|."""
+    DT = {"f64": H.F64, "f32": H.F32, "bf16": H.BF16, "i64": H.I64}[dtype]
+    shape, P = (130, 270), 3
+    rng = np.random.default_rng(3)
+    ints = rng.integers(-50, 50, size=shape)
+    vals = {"f64": ints.astype(np.float64), "f32": ints.astype(np.float32),
+            "bf16": synth.int_bf16(5, shape, -50, 50), "i64": ints.astype(np.int64)}[dtype]
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    for be in (h, w):
+        X = be.create(DT, shape)
+        rowp = be.partition(H.ROW, shape)
+        blk = be.partition(H.BLOCK, shape, (3, 5), (120, 250))
+        be.write(X, rowp, vals)
+    for part in (blk, rowp):
+        for op in (H.SUM, H.MAX, H.MIN):
+            g = h.reduce(X, part, op)
+            o = w.reduce(X, part, op)
+            assert g == o, (op, g, o)
+            assert_same_msgs(h, w)
+    if dtype == "f64":
+        r = synth.uniform(7, shape)
+        for be in (h, w):
+            be.write(X, rowp, r)
+        g, o = h.reduce(X, blk, H.SUM), w.reduce(X, blk, H.SUM)
+        assert abs(g - o) <= 1e-12 * np.abs(r).sum()
+        p2 = np.where(synth.uniform(8, shape) < 0.5, 0.5, 2.0)
+        for be in (h, w):
+            be.write(X, rowp, p2)
+        assert h.reduce(X, rowp, H.PROD) == w.reduce(X, rowp, H.PROD)  # powers of two: exact
+    h.close()

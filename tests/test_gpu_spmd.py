@@ -76,6 +76,14 @@ def _worker(rank, world, port, q):
                 be.apply(H.K_SCALE, cp, [(Z, [(0, 0)], [(0, 0)])], [2.0])
                 be.apply(H.K_SCALE, rp, [(Z, [(0, 0)], [(0, 0)])], [0.5])
         check("bulk", [Z])
+        # Reduce over NVLink sync words: every rank gets the oracle's value
+        ints = np.arange(np.prod(shape), dtype=np.float64).reshape(shape) % 97
+        for be in (h, w):
+            be.write(X, full, ints)
+        for op in (H.SUM, H.MAX, H.MIN):
+            g, o = h.reduce(X, colp, op), w.reduce(X, colp, op)
+            if g != o:
+                bad.append(("reduce", op, g, o))
         got = h.read(X, full)
         ref = w.read(X, full)
         lb, ub = h.region(full, rank, 2)

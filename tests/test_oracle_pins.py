@@ -550,3 +550,84 @@ def test_read_after_write_same_partition_is_local(oracle_mod):
     w.write(X, part, v)
     np.testing.assert_array_equal(w.read(X, part), v)
     assert len(w.msgs()) == 0
+
+
+# ---------------------------------------------------------------------------
+# Reduce (Table 2): closed forms after a redistribution
+# ---------------------------------------------------------------------------
+def test_reduce_closed_forms(oracle_mod):
+    O = oracle_mod
+    n0, n1, P = 12, 10, 3
+    i = np.arange(n0)[:, None]
+    j = np.arange(n1)[None, :]
+    u = (i * n1 + j + 1).astype(np.float64)  # 1 .. n0*n1
+    w = O.Oracle(P)
+    X = w.create(O.F64, (n0, n1))
+    rowp = w.partition(O.ROW, (n0, n1))
+    colp = w.partition(O.COL, (n0, n1))
+    inner = w.partition(O.BLOCK, (n0, n1), (2, 3), (9, 8))
+    w.write(X, rowp, u)
+    N = n0 * n1
+    assert w.reduce(X, colp, O.SUM) == N * (N + 1) / 2       # Gauss
+    assert len(w.msgs()) > 0                                 # coherence moved data (ROW -> COL)
+    assert w.reduce(X, colp, O.MAX) == N and w.reduce(X, colp, O.MIN) == 1
+    sub = u[2:9, 3:8]
+    assert w.reduce(X, inner, O.SUM) == sub.sum() and w.reduce(X, inner, O.MAX) == sub.max()
+    # PROD of powers of two is exact: 2^(sum of exponents)
+    e = ((i + j) % 5 - 2).astype(np.float64)
+    w.write(X, rowp, 2.0 ** e)
+    assert w.reduce(X, rowp, O.PROD) == 2.0 ** e.sum()
+    Y = w.create(O.I64, (n0, n1))
+    w.write(Y, colp, -(i * n1 + j).astype(np.int64))
+    assert w.reduce(Y, rowp, O.SUM) == -(N - 1) * N / 2 and w.reduce(Y, rowp, O.MIN) == -(N - 1)
+
+
+# ---------------------------------------------------------------------------
+# absolute sections + trapezoids (Table 1 use@/def@, Table 2 SetAbsolute*/SetTrapezoid*)
+# ---------------------------------------------------------------------------
+def test_trapezoid_closed_forms(oracle_mod):
+    O = oracle_mod
+    # upper-triangular n x n incl. diagonal: row r spans [r, n-1] -> n(n+1)/2 cells
+    n = 9
+    boxes = O.trapezoid([(0, 0), (0, n - 1), (n - 1, n - 1), (n - 1, n - 1)])
+    assert len(boxes) == n and sum(u[1] - l[1] for l, u in boxes) == n * (n + 1) // 2
+    assert boxes[3] == ((3, 3), (4, n))
+    # lower triangle: row r spans [0, r]
+    boxes = O.trapezoid([(2, 0), (2, 0), (6, 0), (6, 4)])
+    assert [(l[1], u[1]) for l, u in boxes] == [(0, 1), (0, 2), (0, 3), (0, 4), (0, 5)]
+    # rectangle, and a single row
+    assert O.trapezoid([(1, 2), (1, 5), (3, 2), (3, 5)]) == [((r, 2), (r + 1, 6)) for r in (1, 2, 3)]
+    assert O.trapezoid([(4, 1), (4, 3), (4, 1), (4, 3)]) == [((4, 1), (5, 4))]
+    # round half up on the interpolated edge: width 3 over 2 steps -> 0, 2 (1.5 -> 2), 3
+    assert [l[1] for l, _ in O.trapezoid([(0, 0), (0, 9), (2, 3), (2, 9)])] == [0, 2, 3]
+
+
+def test_absolute_sections_triangular(oracle_mod):
+    """Correlation-style symmetric fill: device p defines the
+    upper-triangle rows of its manual row block, then every device uses the full
+    rows of the mirrored lower triangle -> only defined-elsewhere cells move."""
+    O = oracle_mod
+    n, P = 12, 2
+    w = O.Oracle(P)
+    X = w.create(O.F64, (n, n))
+    part = w.partition_manual((n, n), [[0, 0], [4, 0]], [[4, n], [n, n]])  # Listing 1 style (R2)
+    up = O.trapezoid([(0, 0), (0, n - 1), (n - 1, n - 1), (n - 1, n - 1)])
+    defs = [[b for b in up if b[0][0] < 4], [b for b in up if b[0][0] >= 4]]
+    uses = [[((0, 0), (4, n))], [((4, 0), (n, n))]]
+    w.apply_abs(O.K_STAMP, part, [(X, [[], []], defs)], [3.0])
+    own = w.owner_map(X)
+    assert (own[np.triu_indices(n)] == np.where(np.triu_indices(n)[0] < 4, 0, 1)).all()
+    assert (own[np.tril_indices(n, -1)] == -1).all()
+    w.apply_abs(O.K_NONE, part, [(X, uses, [[], []])])
+    m = w.msgs()
+    # device 0 (rows 0-3) owns all of its rows' upper part: nothing to receive;
+    # device 1 (rows 4-11) owns its upper part too: the triangles never cross
+    assert len(m) == 0
+    # now device 1 reads all rows: it needs device 0's triangle rows 0-3 (cols r..n-1)
+    w.apply_abs(O.K_NONE, part, [(X, [[], [((0, 0), (n, n))]], [[], []])])
+    cells = set(int(c) for c in w.msgs()[:, 3])
+    expect = {r * n + c for r in range(4) for c in range(r, n)}
+    assert cells == expect
+    with pytest.raises(O.OracleError) as e:
+        w.apply_abs(O.K_NONE, part, [(X, [[], []], [[((0, 0), (2, 2))], [((1, 1), (3, 3))]])])
+    assert e.value.code == O.ERACE
