@@ -219,6 +219,29 @@ int hda_partition_region(const hda_ctx_t* ctx, hda_part_t part, int32_t dev,
  * scalars: kernel scalars (see enum hda_kernel). Asynchronous w.r.t. the GPUs. */
 int hda_apply(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const hda_access_t* acc,
               int32_t n_acc, const double* scalars, int32_t n_scalars);
+/* Absolute sections (Table 1 use@/def@; Table 2 SetAbsoluteUse/Def, P:L171-173,
+ * P:L188-191): entry i names, per device q, the exact boxes it uses
+ * (n_use[q] boxes) and defines (n_def[q] boxes) in this call, instead of offsets —
+ * for non-rectangular or device-specific access (triangular Correlation-style
+ * kernels).  Boxes: lb[ndim] then ub[ndim] (half-open), device-major.
+ * n_use / n_def may be NULL (none).  Only HDA_K_NONE and HDA_K_STAMP (their device
+ * code has no fixed footprint).  ERANGE if a box leaves the array; ERACE as usual. */
+typedef struct {
+  hda_array_t array;
+  const int32_t* n_use; /* [P] */
+  const int64_t* use;
+  const int32_t* n_def; /* [P] */
+  const int64_t* def;
+} hda_abs_access_t;
+int hda_apply_abs(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const hda_abs_access_t* acc,
+                  int32_t n_acc, const double* scalars, int32_t n_scalars);
+/* Trapezoid helper (Table 2 SetTrapezoidUse/Def): corners =
+ * {top, ul_col, top, ur_col, bottom, bl_col, bottom, br_col} (inclusive cells); writes
+ * one 2-D box {r, left, r+1, right+1} per row with left <= right, edges interpolated
+ * linearly and rounded half up (reading R20).  *n_out = number of rows produced
+ * (boxes may be NULL to query).  Pass the boxes to hda_apply_abs. */
+int hda_trapezoid(const int64_t* corners, int64_t* boxes, int32_t cap, int32_t* n_out);
+
 /* block until every local device has finished all enqueued work */
 int hda_sync(hda_ctx_t* ctx);
 

@@ -4,4 +4,4 @@ The product is libhdarray.so (C-ABI in include/hdarray.h, CUDA for sm_100a);
 this package is its thin ctypes binding.  See DESIGN.md.
 """
 from .hdarray import *  # noqa: F401,F403
-from .hdarray import HDArray, HDAError, lib, plan_cells  # noqa: F401
+from .hdarray import HDArray, HDAError, lib, plan_cells, trapezoid  # noqa: F401

@@ -1306,6 +1306,54 @@ int hda_apply(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const hda_access_
   return call(ctx, kernel, part, in, n_acc, scalars, n_scalars, nullptr, nullptr);
 }
 
+int hda_apply_abs(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const hda_abs_access_t* acc, int32_t n_acc,
+                  const double* scalars, int32_t n_scalars) {
+  GUARD();
+  if (kernel < 0 || kernel >= KN_COUNT) return fail(ctx, HDA_EINVAL, "unknown kernel");
+  if (n_acc < 1 || n_acc > 64 || !acc) return fail(ctx, HDA_EINVAL, "bad access list");
+  if (n_scalars < 0 || (n_scalars && !scalars)) return fail(ctx, HDA_EINVAL, "bad scalars");
+  AccessIn in[64];
+  static const int32_t zeros[HDA_MAX_DEVICES] = {0};
+  for (int i = 0; i < n_acc; i++) {
+    in[i] = AccessIn{acc[i].array, 0, nullptr, 0, nullptr};
+    in[i].n_use_abs = acc[i].n_use ? acc[i].n_use : zeros;
+    in[i].use_abs = acc[i].use;
+    in[i].n_def_abs = acc[i].n_def ? acc[i].n_def : zeros;
+    in[i].def_abs = acc[i].def;
+  }
+  return call(ctx, kernel, part, in, n_acc, scalars, n_scalars, nullptr, nullptr);
+}
+
+// Table 2 SetTrapezoidUse/Def rasterized to per-row boxes
+// (reading R20: inclusive corners, row edges interpolated and rounded half up)
+static int64_t floordiv64(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  if ((a % b) != 0 && ((a < 0) != (b < 0))) q--;
+  return q;
+}
+
+int hda_trapezoid(const int64_t* c, int64_t* boxes, int32_t cap, int32_t* n_out) {
+  if (!c || !n_out) return HDA_EINVAL;
+  const int64_t top = c[0], bottom = c[4];
+  if (c[2] != top || c[6] != bottom || bottom < top) return HDA_EINVAL;
+  const int64_t h = bottom - top;
+  int32_t n = 0;
+  for (int64_t r = top; r <= bottom; r++) {
+    const int64_t left = h ? c[1] + floordiv64((r - top) * (c[5] - c[1]) * 2 + h, 2 * h) : c[1];
+    const int64_t right = h ? c[3] + floordiv64((r - top) * (c[7] - c[3]) * 2 + h, 2 * h) : c[3];
+    if (left > right) continue;
+    if (boxes && n < cap) {
+      boxes[4 * n + 0] = r;
+      boxes[4 * n + 1] = left;
+      boxes[4 * n + 2] = r + 1;
+      boxes[4 * n + 3] = right + 1;
+    }
+    n++;
+  }
+  *n_out = n;
+  return HDA_OK;
+}
+
 int hda_sync(hda_ctx_t* ctx) {
   GUARD();
   if (ctx->plan_only) return HDA_OK;

@@ -256,6 +256,12 @@ int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* 
       return HDA_EINVAL;
     }
   }
+  bool any_abs = false;
+  for (int e = 0; e < n_acc; e++) any_abs |= acc[e].absolute();
+  if (any_abs && kernel != KN_NONE && kernel != KN_STAMP) {
+    err = "absolute sections are for kernels without a fixed footprint (NONE, STAMP)";
+    return HDA_EINVAL;
+  }
   const bool builtin = kernel > KN_NONE && kernel != KN_STAMP;
   if (builtin) {
     if (!(acc[0].n_def == 1 && zero_tuple(acc[0].def, nd))) {
@@ -277,11 +283,15 @@ int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* 
       err = "STAMP needs at least the stamped array";
       return HDA_EINVAL;
     }
-    for (int e = 1; e < n_acc; e++)
-      if (acc[e].n_def) {
+    for (int e = 1; e < n_acc; e++) {
+      bool d = acc[e].n_def != 0;
+      if (acc[e].n_def_abs)
+        for (int q = 0; q < P_; q++) d |= acc[e].n_def_abs[q] != 0;
+      if (d) {
         err = "STAMP defines only parameter 0";
         return HDA_EINVAL;
       }
+    }
   }
   if (kernel == KN_GEMM && n_scalars < 2) {
     err = "GEMM needs scalars {alpha, beta}";
@@ -404,6 +414,7 @@ int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* 
   // used at a non-zero offset and defined in the same call (reading R15)
   for (int e = 0; e < n_acc; e++)
     for (int f = 0; f < n_acc; f++) {
+      if (acc[e].absolute() || acc[f].absolute()) continue;
       if (acc[e].array != acc[f].array || !acc[f].n_def) continue;
       for (int t = 0; t < acc[e].n_use; t++)
         if (!zero_tuple(acc[e].use + (size_t)t * nd, nd)) {
@@ -432,6 +443,28 @@ int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* 
       std::vector<Box> u, df;
       for (int e = 0; e < n_acc; e++) {
         if (acc[e].array != X) continue;
+        if (acc[e].absolute()) {  // explicit per-device sections
+          for (int pass = 0; pass < 2; pass++) {
+            const int32_t* cnt = pass ? acc[e].n_def_abs : acc[e].n_use_abs;
+            const int64_t* bx = pass ? acc[e].def_abs : acc[e].use_abs;
+            if (!cnt) continue;
+            int64_t off = 0;
+            for (int q = 0; q < d; q++) off += (int64_t)cnt[q] * 2 * nd;
+            for (int32_t b = 0; b < cnt[d]; b++) {
+              Box bb = unit_box();
+              for (int kk = 0; kk < nd; kk++) {
+                bb.lb[kk] = bx[off + (int64_t)b * 2 * nd + kk];
+                bb.ub[kk] = bx[off + (int64_t)b * 2 * nd + nd + kk];
+                if (bb.lb[kk] < 0 || bb.ub[kk] > a.shape[kk] || bb.lb[kk] > bb.ub[kk]) {
+                  err = "absolute section outside the array";
+                  return HDA_ERANGE;
+                }
+              }
+              (pass ? df : u).push_back(bb);
+            }
+          }
+          continue;
+        }
         Rects cu = compose(acc[e].use, acc[e].n_use, nd, pt.box[d], a.shape);
         Rects cd = compose(acc[e].def, acc[e].n_def, nd, pt.box[d], a.shape);
         u.insert(u.end(), cu.begin(), cu.end());
@@ -562,6 +595,21 @@ int Tracker::plan(int32_t kernel, int32_t part, const AccessIn* acc, int32_t n_a
       return HDA_EINVAL;
     }
     int nd = arrays_[acc[e].array].ndim;
+    key.push_back(acc[e].absolute() ? 1 : 0);
+    if (acc[e].absolute()) {
+      for (int pass = 0; pass < 2; pass++) {
+        const int32_t* cnt = pass ? acc[e].n_def_abs : acc[e].n_use_abs;
+        const int64_t* bx = pass ? acc[e].def_abs : acc[e].use_abs;
+        int64_t off = 0;
+        for (int q = 0; q < P_; q++) {
+          int32_t n = cnt ? cnt[q] : 0;
+          key.push_back(n);
+          for (int64_t i = 0; i < (int64_t)n * 2 * nd; i++) key.push_back(bx[off + i]);
+          off += (int64_t)n * 2 * nd;
+        }
+      }
+      continue;
+    }
     key.push_back(acc[e].n_use);
     for (int i = 0; i < acc[e].n_use * nd && acc[e].use; i++) key.push_back(acc[e].use[i]);
     key.push_back(acc[e].n_def);

@@ -78,6 +78,13 @@ struct AccessIn {  // one access-list entry, as passed through the C-ABI
   const int32_t* use;
   int32_t n_def;
   const int32_t* def;
+  // absolute sections (Table 1 use@/def@): per-device box counts [P] and boxes
+  // (lb[ndim], ub[ndim] each, device-major); when set, the offsets are ignored
+  const int32_t* n_use_abs = nullptr;
+  const int64_t* use_abs = nullptr;
+  const int32_t* n_def_abs = nullptr;
+  const int64_t* def_abs = nullptr;
+  bool absolute() const { return n_use_abs != nullptr || n_def_abs != nullptr; }
 };
 
 // state-independent facts about a call spec, validated once

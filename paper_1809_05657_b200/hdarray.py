@@ -32,6 +32,12 @@ class hda_access_t(ctypes.Structure):
                 ("n_def", ctypes.c_int32), ("def_", ctypes.POINTER(ctypes.c_int32))]
 
 
+class hda_abs_access_t(ctypes.Structure):
+    _fields_ = [("array", ctypes.c_int32), ("n_use", ctypes.POINTER(ctypes.c_int32)),
+                ("use", ctypes.POINTER(ctypes.c_int64)), ("n_def", ctypes.POINTER(ctypes.c_int32)),
+                ("def_", ctypes.POINTER(ctypes.c_int64))]
+
+
 class hda_msg_t(ctypes.Structure):
     _fields_ = [("array", ctypes.c_int32), ("src", ctypes.c_int32), ("dst", ctypes.c_int32),
                 ("ndim", ctypes.c_int32), ("lb", ctypes.c_int64 * 3), ("ub", ctypes.c_int64 * 3)]
@@ -46,7 +52,7 @@ class hda_stats_t(ctypes.Structure):
 EXPORTS = [
     "hda_init", "hda_init_spmd", "hda_finalize", "hda_num_devices", "hda_is_local", "hda_spmd_export",
     "hda_spmd_import", "hda_create", "hda_create_ext", "hda_free", "hda_device_ptr", "hda_partition",
-    "hda_partition_manual", "hda_partition_region", "hda_apply", "hda_sync", "hda_write", "hda_read", "hda_reduce",
+    "hda_partition_manual", "hda_partition_region", "hda_apply", "hda_apply_abs", "hda_trapezoid", "hda_sync", "hda_write", "hda_read", "hda_reduce",
     "hda_set_transport", "hda_set_overlap", "hda_set_plan_cache", "hda_set_kernel_timing", "hda_kernel_time", "hda_exchange_time",
     "hda_stream", "hda_last_plan", "hda_owner_map", "hda_read_replica", "hda_stats", "hda_reset_stats",
     "hda_last_error", "hda_version",
@@ -82,6 +88,8 @@ def lib():
             "hda_partition_region": [vp, i32, i32, P(i64), P(i64)],
             "hda_apply": [vp, i32, i32, P(hda_access_t), i32, P(ctypes.c_double), i32],
             "hda_sync": [vp],
+            "hda_apply_abs": [vp, i32, i32, P(hda_abs_access_t), i32, P(ctypes.c_double), i32],
+            "hda_trapezoid": [P(i64), P(i64), i32, P(i32)],
             "hda_write": [vp, i32, i32, vp],
             "hda_read": [vp, i32, i32, vp],
             "hda_reduce": [vp, i32, i32, i32, P(ctypes.c_double)],
@@ -249,6 +257,24 @@ class HDArray:
         sc = (ctypes.c_double * max(len(scalars), 1))(*[float(s) for s in scalars])
         self._chk(self.L.hda_apply(self.h, kernel, part, entries, n, sc, len(scalars)))
 
+    def apply_abs(self, kernel, part, acc, scalars=()):
+        """acc: list of (array, uses, defs); uses/defs: per device a list of boxes
+        ((lb...), (ub...)) — absolute sections (Table 1 use@/def@)."""
+        n = len(acc)
+        entries = (hda_abs_access_t * n)()
+        keep = []
+        for i, (a, uses, defs) in enumerate(acc):
+            for fld_n, fld_b, lists in (("n_use", "use", uses), ("n_def", "def_", defs)):
+                cnt = (ctypes.c_int32 * self.P)(*[len(lists[q]) for q in range(self.P)])
+                flat = [int(v) for q in range(self.P) for lb, ub in lists[q] for v in list(lb) + list(ub)]
+                arr = (ctypes.c_int64 * max(len(flat), 1))(*flat)
+                keep += [cnt, arr]
+                setattr(entries[i], fld_n, ctypes.cast(cnt, ctypes.POINTER(ctypes.c_int32)))
+                setattr(entries[i], fld_b, ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64)))
+            entries[i].array = a
+        sc = (ctypes.c_double * max(len(scalars), 1))(*[float(s) for s in scalars])
+        self._chk(self.L.hda_apply_abs(self.h, kernel, part, entries, n, sc, len(scalars)))
+
     def sync(self):
         self._chk(self.L.hda_sync(self.h))
 
@@ -338,6 +364,19 @@ class HDArray:
 
     def reset_stats(self):
         self._chk(self.L.hda_reset_stats(self.h))
+
+
+def trapezoid(corners):
+    """per-row 2-D boxes of a trapezoid, corners [(top,ul),(top,ur),(bottom,bl),(bottom,br)]."""
+    L = lib()
+    c = (ctypes.c_int64 * 8)(*[int(x) for cc in corners for x in cc])
+    n = ctypes.c_int32()
+    rc = L.hda_trapezoid(c, None, 0, ctypes.byref(n))
+    if rc:
+        raise HDAError(rc, "bad trapezoid corners")
+    out = (ctypes.c_int64 * max(4 * n.value, 4))()
+    L.hda_trapezoid(c, out, n.value, ctypes.byref(n))
+    return [((out[4 * i], out[4 * i + 1]), (out[4 * i + 2], out[4 * i + 3])) for i in range(n.value)]
 
 
 def plan_cells(plan, shapes):

@@ -430,3 +430,27 @@ def test_reduce_vs_oracle(H, dtype):
             be.write(X, rowp, p2)
         assert h.reduce(X, rowp, H.PROD) == w.reduce(X, rowp, H.PROD)  # powers of two: exact
     h.close()
+
+
+# ------------------------------------------------------------------ absolute sections (§8(f)-2)
+def test_absolute_sections_triangular_gpu(H):
+    """Correlation-style triangular access with a Listing-1 manual partition
+    (P:L197-208): each device STAMPs the upper-triangle rows of its slab,
+    then every device reads the whole upper triangle; replicas bit-exact vs oracle."""
+    n, P = 96, 2
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    up = H.trapezoid([(0, 0), (0, n - 1), (n - 1, n - 1), (n - 1, n - 1)])
+    cut = 28  # ~ n(1 - 1/sqrt 2): halves the triangle's work (Listing 1's 3008/10240)
+    defs = [[b for b in up if b[0][0] < cut], [b for b in up if b[0][0] >= cut]]
+    for be in (h, w):
+        X = be.create(H.F64, (n, n))
+        part = be.partition_manual((n, n), [[0, 0], [cut, 0]], [[cut, n], [n, n]])
+    for be in (h, w):
+        be.apply_abs(H.K_STAMP, part, [(X, [[], []], defs)], [9.0])
+    for be in (h, w):
+        be.apply_abs(H.K_NONE, part, [(X, [up, up], [[], []])])
+    assert_same_msgs(h, w)
+    assert len(w.msgs()) > 0
+    assert_replicas(h, w, [X], P)
+    h.close()

@@ -142,3 +142,57 @@ def test_table3_closed_forms_at_paper_scale():
     assert vols[2:] == [per_sweep] * 3
     assert round(_gib(1e5 * per_sweep)) == 473
     assert h.stats()["plan_hits"] >= 4
+
+
+def test_trapezoid_helper_matches_oracle():
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        top = int(rng.integers(0, 20))
+        bottom = top + int(rng.integers(0, 15))
+        c = [(top, int(rng.integers(0, 30))), (top, int(rng.integers(0, 30))),
+             (bottom, int(rng.integers(0, 30))), (bottom, int(rng.integers(0, 30)))]
+        assert H.trapezoid(c) == O.trapezoid(c), c
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_absolute_sections_random(P):
+    """Random per-device absolute sections (triangles, rectangles) for uses and defs:
+    message element sets and owner maps equal to the oracle."""
+    rng = np.random.default_rng(100 + P)
+    n = 16
+    for trial in range(25):
+        w = O.Oracle(P, with_data=False)
+        h = H.HDArray(n_gpus=0, n_devices=P)
+        parts = []
+        for be in (w, h):
+            X = be.create(H.F64, (n, n))
+            parts.append(be.partition(H.ROW, (n, n)))
+        # disjoint defs: row slabs, each a trapezoid clipped to its slab
+        cuts = np.sort(rng.integers(0, n + 1, P - 1))
+        bounds = [0] + list(cuts) + [n]
+        for step in range(4):
+            defs, uses = [], []
+            for q in range(P):
+                r0, r1 = int(bounds[q]), int(bounds[q + 1])
+                if r1 > r0 and rng.random() < 0.8:
+                    c = [(r0, int(rng.integers(0, n))), (r0, int(rng.integers(0, n))),
+                         (r1 - 1, int(rng.integers(0, n))), (r1 - 1, int(rng.integers(0, n)))]
+                    defs.append(H.trapezoid(c))
+                else:
+                    defs.append([])
+                ub = []
+                for _ in range(int(rng.integers(0, 3))):
+                    a0, a1 = sorted(rng.integers(0, n + 1, 2))
+                    b0, b1 = sorted(rng.integers(0, n + 1, 2))
+                    ub.append(((int(a0), int(b0)), (int(a1), int(b1))))
+                uses.append(ub)
+            w.apply_abs(O.K_NONE, parts[0], [(X, uses, defs)])
+            h.apply_abs(H.K_NONE, parts[1], [(X, uses, defs)])
+            mo = O.msgs_by_pair(w.msgs())
+            from programs import LibAdapter
+            ml = O.msgs_by_pair(LibAdapter(h).msgs())
+            assert mo.keys() == ml.keys()
+            for k in mo:
+                np.testing.assert_array_equal(mo[k], ml[k])
+            np.testing.assert_array_equal(w.owner_map(X), h.owner_map(X))
+        h.close()
