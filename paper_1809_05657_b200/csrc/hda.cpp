@@ -689,24 +689,69 @@ static int sync_only(hda_ctx_t* ctx, int q, const KSync& ks) {
   return HDA_OK;
 }
 
+// launch the built-in kernel of call t on device q over `boxes` (default: q's work box)
+// in as few launches as possible; waits ride with the first launch, signals with the last
+static KSync ks_part(hda_ctx_t* ctx, const KSync& ks, bool first, bool last) {
+  KSync k2 = ks_empty(ctx);
+  if (first) {
+    std::memcpy(k2.wait_ptr, ks.wait_ptr, sizeof k2.wait_ptr);
+    std::memcpy(k2.wait_val, ks.wait_val, sizeof k2.wait_val);
+    k2.nwait = ks.nwait;
+  }
+  if (last) {
+    std::memcpy(k2.sig_ptr, ks.sig_ptr, sizeof k2.sig_ptr);
+    k2.nsig = ks.nsig;
+    k2.sig_val = ks.sig_val;
+    k2.ctr = ks.ctr;
+  }
+  return k2;
+}
+
 static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
-                      const Box* wbox = nullptr) {
+                      const std::vector<Box>* boxes = nullptr) {
   const CallInfo& ci = *t->info;
   const TPart& pt = ctx->tr->part(ci.part);
   const int X0 = ci.param_array[0];
   const TArray& a0 = ctx->tr->array(X0);
   int64_t S[3];
   front_shape(a0.ndim, a0.shape, S);
-  const Box fb = front_box(a0.ndim, wbox ? *wbox : pt.box[q]);
+  std::vector<Box> fbs;
+  if (boxes) {
+    for (const Box& b : *boxes) fbs.push_back(front_box(a0.ndim, b));
+  } else {
+    fbs.push_back(front_box(a0.ndim, pt.box[q]));
+  }
+  const Box fb = fbs.empty() ? front_box(a0.ndim, pt.box[q]) : fbs[0];
   cudaStream_t s = stream_of(ctx, q);
   auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
+  if (ci.kernel == KN_JACOBI5 || ci.kernel == KN_STENCIL9) {
+    const size_t nb = fbs.size();
+    for (size_t i0 = 0; i0 < std::max<size_t>(nb, 1); i0 += 8) {
+      const int64_t* lbs[8];
+      const int64_t* ubs[8];
+      int n = 0;
+      for (size_t i = i0; i < nb && n < 8; i++, n++) {
+        lbs[n] = fbs[i].lb;
+        ubs[n] = fbs[i].ub;
+      }
+      const KSync k2 = ks_part(ctx, ks, i0 == 0, i0 + 8 >= nb);
+      if (ci.kernel == KN_JACOBI5)
+        CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, lbs, ubs, n, k2, s));
+      else
+        CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, lbs, ubs, n, k2, s));
+      count_launch(ctx);
+    }
+    return HDA_OK;
+  }
+  if (fbs.size() > 1 && (ci.kernel == KN_STENCIL7_3D || ci.kernel == KN_SCALE || ci.kernel == KN_COPY)) {
+    for (size_t i = 0; i < fbs.size(); i++) {
+      std::vector<Box> one{boxes->at(i)};
+      int rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, i == 0, i + 1 == fbs.size()), &one);
+      if (rc) return rc;
+    }
+    return HDA_OK;
+  }
   switch (ci.kernel) {
-    case KN_JACOBI5:
-      CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, ks, s));
-      break;
-    case KN_STENCIL9:
-      CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, ks, s));
-      break;
     case KN_STENCIL7_3D:
       CK(launch_stencil7(a0.dtype, P_(1), P_(0), S, fb.lb, fb.ub, ks, s));
       break;
@@ -884,34 +929,25 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
         if ((rc = sync_only(ctx, q, post))) return rc;
       } else if (kern && ctx->pulled_on_comm[q]) {
-        // interior boxes while the pull is in flight, dependent boxes after it
+        // interior boxes while the pull is in flight, dependent boxes after it (one
+        // launch each for the 2-D stencils)
         const PullJob& job = *ctx->cur_pull[q];
         Gpu& g = ctx->gpus[ctx->dev[q].gpu];
-        std::vector<std::pair<const Box*, bool>> seq;  // (box, after the pull)
-        for (const Box& b : job.interior) seq.push_back({&b, false});
-        for (const Box& b : job.dependent) seq.push_back({&b, true});
         bool joined = false;
-        for (size_t i = 0; i < seq.size(); i++) {
-          if (seq[i].second && !joined) {
-            CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
-            joined = true;
-          }
-          KSync k2 = ks_empty(ctx);
-          if (i == 0) {
-            std::memcpy(k2.wait_ptr, ks.wait_ptr, sizeof k2.wait_ptr);
-            std::memcpy(k2.wait_val, ks.wait_val, sizeof k2.wait_val);
-            k2.nwait = ks.nwait;
-          }
-          if (i + 1 == seq.size()) {
-            std::memcpy(k2.sig_ptr, ks.sig_ptr, sizeof k2.sig_ptr);
-            k2.nsig = ks.nsig;
-            k2.sig_val = ks.sig_val;
-            k2.ctr = ks.ctr;
-          }
+        const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
+        if (has_i) {
           cudaEvent_t a;
           if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-          if ((rc = run_kernel(ctx, t, q, scalars, k2, seq[i].first))) return rc;
-          if ((rc = timed_end(ctx, g.stream, kernel, a, i == 0 ? 1 : 0))) return rc;
+          if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, true, !has_d), &job.interior))) return rc;
+          if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
+        }
+        if (has_d) {
+          CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+          joined = true;
+          cudaEvent_t a;
+          if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+          if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, !has_i, true), &job.dependent))) return rc;
+          if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
         }
         if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
         ctx->pulled_on_comm[q] = 0;

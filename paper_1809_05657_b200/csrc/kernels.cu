@@ -235,14 +235,17 @@ __device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
 }
 
 // KIND 0 = JACOBI5, 1 = STENCIL9
+// up to 8 boxes per launch (blockIdx.z picks the box): the dependent boundary strips of
+// an overlapped halo exchange run as ONE launch
+struct Boxes2 {
+  int64_t r0[8], r1[8], c0[8], c1[8], cbase[8];
+  int32_t gx[8], gy[8];
+  int32_t n;
+};
+
 template <typename T, int KIND, int ROWS>
-__global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST_MINB - 1 : ST_MINB)
-    stencil2d_kernel(const T* __restrict__ in,
-                                                             T* __restrict__ out, int64_t ld,
-                                                             int64_t r0, int64_t r1, int64_t c0,
-                                                             int64_t c1, int64_t cbase,
-                                                             const __grid_constant__ KSync ks) {
-  ks_pre(ks);
+__device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
+                                               int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase) {
   constexpr int V = V16<T>::n;
   constexpr int W = ST_GROUP + 2;
   const int lane = threadIdx.x & 31;
@@ -330,6 +333,16 @@ __global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST
       rgt[1] = rgt[ST_GROUP + 1];
     }
   }
+}
+
+template <typename T, int KIND, int ROWS>
+__global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST_MINB - 1 : ST_MINB)
+    stencil2d_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld, const __grid_constant__ Boxes2 bx,
+                     const __grid_constant__ KSync ks) {
+  ks_pre(ks);
+  const int b = blockIdx.z;
+  if ((int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b])  // block-uniform
+    stencil2d_body<T, KIND, ROWS>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b]);
   ks_post(ks);
 }
 
@@ -353,39 +366,64 @@ __global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict_
 }
 
 template <typename T, int KIND>
-static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* lb,
-                                      const int64_t* ub, const KSync& ks, cudaStream_t s) {
+static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* const* lbs,
+                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
   const int64_t ld = shape[2];
-  const int64_t r0 = lb[1], r1 = ub[1], c0 = lb[2], c1 = ub[2];
-  if (r0 >= r1 || c0 >= c1 || lb[0] >= ub[0]) return cudaSuccess;
   constexpr int V = V16<T>::n;
   const bool vec = (ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
                    ((uintptr_t)out % 16) == 0;
   if (vec) {
     constexpr int ROWS = ST_ROWS;
-    const int64_t cbase = c0 - (c0 % V);
-    const int64_t per_block = (int64_t)ST_THREADS * V;
-    dim3 grid((unsigned)((c1 - cbase + per_block - 1) / per_block), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));
-    stencil2d_kernel<T, KIND, ROWS><<<grid, ST_THREADS, 0, s>>>(in, out, ld, r0, r1, c0, c1, cbase, ks);
+    Boxes2 bx;
+    bx.n = 0;
+    int gx = 1, gy = 1;
+    for (int i = 0; i < nb; i++) {
+      const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
+      if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
+      const int k = bx.n++;
+      bx.r0[k] = r0;
+      bx.r1[k] = r1;
+      bx.c0[k] = c0;
+      bx.c1[k] = c1;
+      bx.cbase[k] = c0 - (c0 % V);
+      const int64_t per_block = (int64_t)ST_THREADS * V;
+      bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
+      bx.gy[k] = (int)((r1 - r0 + ROWS - 1) / ROWS);
+      gx = std::max(gx, bx.gx[k]);
+      gy = std::max(gy, bx.gy[k]);
+    }
+    if (bx.n == 0) {  // nothing to compute, but the sync words must still move
+      bx.n = 1;
+      bx.gx[0] = bx.gy[0] = 0;
+    }
+    stencil2d_kernel<T, KIND, ROWS><<<dim3(gx, gy, bx.n), ST_THREADS, 0, s>>>(in, out, ld, bx, ks);
   } else {
-    dim3 grid((unsigned)((c1 - c0 + 127) / 128), (unsigned)(r1 - r0));
-    stencil2d_scalar_kernel<T, KIND><<<grid, 128, 0, s>>>(in, out, ld, r0, r1, c0, c1, ks);
+    for (int i = 0; i < nb; i++) {
+      const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
+      if (r0 >= r1 || c0 >= c1) continue;
+      // scalar fallback (test shapes): sync words ride with the first/last launch
+      KSync k2 = ks;
+      if (i != 0) k2.nwait = 0;
+      if (i != nb - 1) k2.nsig = 0;
+      dim3 grid((unsigned)((c1 - c0 + 127) / 128), (unsigned)(r1 - r0));
+      stencil2d_scalar_kernel<T, KIND><<<grid, 128, 0, s>>>(in, out, ld, r0, r1, c0, c1, k2);
+    }
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
-                           const int64_t* ub, const KSync& ks, cudaStream_t s) {
+cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
+                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
   if (dtype == 0)
-    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lb, ub, ks, s);
-  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lb, ub, ks, s);
+    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
+  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
 }
 
-cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* lb,
-                            const int64_t* ub, const KSync& ks, cudaStream_t s) {
+cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
+                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
   if (dtype == 0)
-    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lb, ub, ks, s);
-  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lb, ub, ks, s);
+    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
+  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
 }
 
 // =====================================================================================

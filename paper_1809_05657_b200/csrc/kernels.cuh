@@ -75,10 +75,13 @@ cudaError_t launch_wait(const WaitList& w, int* err_flag, long long timeout_ns, 
 cudaError_t launch_signal(const SignalList& l, cudaStream_t s);
 
 // user kernels over the work box [lb, ub) of one device's replica (padded 3-D shape)
+// 2-D stencils over nb (<= 8) boxes in ONE launch (lbs[i], ubs[i] front-padded 3-D)
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
-                           const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
+                           const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
+                           cudaStream_t s);
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape,
-                            const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
+                            const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
+                            cudaStream_t s);
 cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb,
