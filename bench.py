@@ -440,13 +440,16 @@ def main():
         ev1 = torch.cuda.Event(enable_timing=True)
         barrier()
         ev0.record(stream)
+        th0 = time.perf_counter()
         for _ in range(args.steps):
             wl.step()
+        host_us = (time.perf_counter() - th0) / args.steps * 1e6
         ev1.record(stream)
         barrier()
         ms = ev0.elapsed_time(ev1)
     else:
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        host_us = None
         barrier()
         for i in range(args.steps):
             with torch.cuda.stream(stream):
@@ -570,7 +573,8 @@ def main():
                          "nvlink_peak_GBps": NVLINK_GBS},
             "parity": par,
             "tracker": {"plan_hits": st["plan_hits"], "plan_misses": st["plan_misses"],
-                        "tracker_us_per_call": st["tracker_us"] / max(st["n_apply"], 1)},
+                        "tracker_us_per_call": st["tracker_us"] / max(st["n_apply"], 1),
+                        "host_issue_us_per_step": host_us},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

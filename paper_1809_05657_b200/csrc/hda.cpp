@@ -559,9 +559,9 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
           post.sig_ptr[post.nsig++] = ctx->dev[p].sync + SW_ACK + q;
         }
       int rc;
-      cudaEvent_t a;
-      if ((rc = timed_begin(ctx, st, &a))) return rc;
+      cudaEvent_t a = nullptr;
       const size_t nb = job.batches.size();
+      if (job.ce.empty() && (rc = timed_begin(ctx, st, &a))) return rc;
       if (!job.ce.empty()) {  // copy-engine part: RAW wait kernel, then the copies
         KSync w = ks_empty(ctx);
         std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
@@ -574,6 +574,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
           count_launch(ctx);
         }
         pre.nwait = 0;
+        if ((rc = timed_begin(ctx, st, &a))) return rc;  // transfer time, not the wait
         for (const cudaMemcpy3DParms& p : job.ce) CK(cudaMemcpy3DAsync(&p, st));
         if (nb == 0) {
           CK(launch_copy_runs(empty, post, st));  // ACK signals after the copies

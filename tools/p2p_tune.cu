@@ -7,6 +7,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #define CK(x)                                                                  \
   do {                                                                         \
@@ -31,7 +32,80 @@ __global__ void __launch_bounds__(256) copy_kernel(const uint4* __restrict__ src
   for (; i < n; i += stride) dst[i] = src[i];
 }
 
+// all-to-all over G GPUs: every GPU pulls `bytes` from each peer (the ROW<->COL
+// repartition); (a) copy engine, one stream; (b) copy engine, one stream per peer;
+// (c) SM pull kernel per peer on one stream.  Time = max over GPUs.
+static void all_to_all(int G, size_t bytes) {
+  std::vector<void*> src(G), dst(G);
+  std::vector<std::vector<cudaStream_t>> st(G, std::vector<cudaStream_t>(G));
+  std::vector<cudaEvent_t> e0(G), e1(G);
+  for (int g = 0; g < G; g++) {
+    CK(cudaSetDevice(g));
+    for (int h = 0; h < G; h++)
+      if (h != g) cudaDeviceEnablePeerAccess(h, 0);
+    cudaGetLastError();
+    CK(cudaMalloc(&src[g], bytes));
+    CK(cudaMalloc(&dst[g], bytes * G));
+    for (int h = 0; h < G; h++) CK(cudaStreamCreateWithFlags(&st[g][h], cudaStreamNonBlocking));
+    cudaEventCreate(&e0[g]);
+    cudaEventCreate(&e1[g]);
+  }
+  const size_t n = bytes / 16;
+  for (int mode = 0; mode < 3; mode++) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; rep++) {
+      for (int g = 0; g < G; g++) {
+        CK(cudaSetDevice(g));
+        CK(cudaDeviceSynchronize());
+      }
+      for (int g = 0; g < G; g++) {
+        CK(cudaSetDevice(g));
+        cudaEventRecord(e0[g], st[g][0]);
+        for (int h = 0; h < G; h++) {
+          if (h == g) continue;
+          cudaStream_t s = mode == 1 ? st[g][h] : st[g][0];
+          if (mode == 1) {
+            cudaStreamWaitEvent(s, e0[g], 0);
+          }
+          if (mode == 2)
+            copy_kernel<4><<<148 * 8, 256, 0, s>>>((const uint4*)src[h], (uint4*)((char*)dst[g] + h * bytes), n);
+          else
+            CK(cudaMemcpyPeerAsync((char*)dst[g] + h * bytes, g, src[h], h, bytes, s));
+        }
+        if (mode == 1)
+          for (int h = 0; h < G; h++)
+            if (h != g && h != 0) {
+              cudaEvent_t ev;
+              cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+              cudaEventRecord(ev, st[g][h]);
+              cudaStreamWaitEvent(st[g][0], ev, 0);
+              cudaEventDestroy(ev);
+            }
+        cudaEventRecord(e1[g], st[g][0]);
+      }
+      float worst = 0;
+      for (int g = 0; g < G; g++) {
+        CK(cudaSetDevice(g));
+        CK(cudaEventSynchronize(e1[g]));
+        float ms;
+        cudaEventElapsedTime(&ms, e0[g], e1[g]);
+        worst = ms > worst ? ms : worst;
+      }
+      best = worst < best ? worst : best;
+    }
+    const char* nm[3] = {"CE one stream", "CE stream per peer", "SM pull x4"};
+    printf("all-to-all G=%d %-22s %8.3f ms  per-GPU in %7.1f GB/s\n", G, nm[mode], best,
+           (G - 1) * bytes / (best * 1e-3) / 1e9);
+  }
+}
+
 int main(int argc, char** argv) {
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  if (argc > 2 && atoi(argv[2]) > 0) {
+    all_to_all(ndev, (size_t)atol(argv[1]) << 20);
+    return 0;
+  }
   const size_t bytes = (argc > 1 ? atol(argv[1]) : 1024L) << 20;  // MiB per direction
   const size_t n = bytes / 16;
   void *a[2], *b[2];

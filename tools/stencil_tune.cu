@@ -72,6 +72,98 @@ __global__ void __launch_bounds__(THREADS, MINB) march(const double* __restrict_
   }
 }
 
+// ------------------------------------------------------------- 9-point variants
+__device__ __forceinline__ double st9(double w, double e, double n, double s, double nw, double ne, double sw,
+                                      double se) {
+  double a = ((w + e) + n) + s;
+  double c = ((nw + ne) + sw) + se;
+  double t = 4.0 * a;
+  t = t + c;
+  return t / 20.0;
+}
+// REC=1: recompute left/right shuffles of up/cur/dn for every output row (no L/R window)
+template <int ROWS, int GROUP, int MINB, int REC>
+__global__ void __launch_bounds__(256, MINB) march9(const double* __restrict__ in, double* __restrict__ out, long ld,
+                                                    long r0, long r1, long c0, long c1, long cbase) {
+  constexpr int W = GROUP + 2;
+  const int lane = threadIdx.x & 31;
+  const long col = cbase + ((long)blockIdx.x * 256 + threadIdx.x) * 2;
+  const bool live = col < ld;
+  const long rs = r0 + (long)blockIdx.y * ROWS;
+  const long re = min(rs + (long)ROWS, r1);
+  double w[W][2], lf[W], rg[W];
+  auto ldr = [&](double(&r)[2], long row) {
+    if (live) {
+      double2 v = __ldg(reinterpret_cast<const double2*>(in + row * ld + col));
+      r[0] = v.x;
+      r[1] = v.y;
+    } else {
+      r[0] = r[1] = 0;
+    }
+  };
+  auto edges = [&](const double(&r)[2], long row, double& L, double& R) {
+    L = __shfl_up_sync(0xffffffffu, r[1], 1);
+    R = __shfl_down_sync(0xffffffffu, r[0], 1);
+    if (lane == 0 && live && col > 0) L = __ldg(in + row * ld + col - 1);
+    if (lane == 31 && live && col + 2 < ld) R = __ldg(in + row * ld + col + 2);
+  };
+  ldr(w[0], rs - 1);
+  ldr(w[1], rs);
+  if (!REC) {
+    edges(w[0], rs - 1, lf[0], rg[0]);
+    edges(w[1], rs, lf[1], rg[1]);
+  }
+  for (long base = rs; base < re; base += GROUP) {
+#pragma unroll
+    for (int k = 0; k < GROUP; k++)
+      if (base + 1 + k <= re) ldr(w[k + 2], base + 1 + k);
+#pragma unroll
+    for (int k = 0; k < GROUP; k++) {
+      const long r = base + k;
+      if (r >= re) break;
+      double ul, ur, cl, cr, dl, dr;
+      if (REC) {
+        edges(w[k], r - 1, ul, ur);
+        edges(w[k + 1], r, cl, cr);
+        edges(w[k + 2], r + 1, dl, dr);
+      } else {
+        edges(w[k + 2], r + 1, lf[k + 2], rg[k + 2]);
+        ul = lf[k];
+        ur = rg[k];
+        cl = lf[k + 1];
+        cr = rg[k + 1];
+        dl = lf[k + 2];
+        dr = rg[k + 2];
+      }
+      const double* up = w[k];
+      const double* cu = w[k + 1];
+      const double* dn = w[k + 2];
+      double o0 = st9(cl, cu[1], up[0], dn[0], ul, up[1], dl, dn[1]);
+      double o1 = st9(cu[0], cr, up[1], dn[1], up[0], ur, dn[0], dr);
+      if (live) {
+        double* d = out + r * ld + col;
+        if (col >= c0 && col + 2 <= c1)
+          *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+        else {
+          if (col >= c0 && col < c1) d[0] = o0;
+          if (col + 1 >= c0 && col + 1 < c1) d[1] = o1;
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 2; v++) {
+      w[0][v] = w[GROUP][v];
+      w[1][v] = w[GROUP + 1][v];
+    }
+    if (!REC) {
+      lf[0] = lf[GROUP];
+      rg[0] = rg[GROUP];
+      lf[1] = lf[GROUP + 1];
+      rg[1] = rg[GROUP + 1];
+    }
+  }
+}
+
 // ------------------------------------------------------------- C: one vector per thread
 __global__ void __launch_bounds__(256) simple(const double* __restrict__ in, double* __restrict__ out, long ld,
                                               long r0, long r1, long c0, long c1, long cbase) {
@@ -220,55 +312,27 @@ int main() {
     march<32, 8, 128, 1><<<g, 128>>>(X, R, n, r0, r1, c0, c1, cbase);
     CK(cudaDeviceSynchronize());
   }
-  time_it("A march R32 G8 T128", [&] {
-    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
-    march<32, 8, 128, 1><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
-  });
-  time_it("B march R32 G4 T128 minB8", [&] {
-    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
-    march<32, 4, 128, 8><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
-  });
-  time_it("B2 march R64 G4 T128 minB8", [&] {
-    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 63) / 64));
-    march<64, 4, 128, 8><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
-  });
-  time_it("B3 march R16 G4 T256 minB4", [&] {
+  time_it("jacobi B3 march R16 G4 T256 minB4", [&] {
     dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + 15) / 16));
     march<16, 4, 256, 4><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);
   });
-  time_it("D march R32 G8 T128 minB6", [&] {
-    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 31) / 32));
-    march<32, 8, 128, 6><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
-  });
-  time_it("D2 march R128 G8 T128 minB6", [&] {
-    dim3 g((unsigned)((c1 - cbase + 255) / 256), (unsigned)((r1 - r0 + 127) / 128));
-    march<128, 8, 128, 6><<<g, 128>>>(X, Y, n, r0, r1, c0, c1, cbase);
-  });
-  time_it("C simple", [&] {
-    dim3 g((unsigned)((c1 - cbase + 127) / 128), (unsigned)((r1 - r0 + 3) / 4));
-    simple<<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);
-  });
-  // E: TMA
-  void* fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-  CUtensorMap map;
-  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
-  cuuint64_t str[1] = {(cuuint64_t)n * 8};
-  cuuint32_t box[2] = {e::BOXW, e::BOXH};
-  cuuint32_t es[2] = {1, 1};
-  CUresult cr = ((EncodeFn)fn)(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, X, dims, str, box, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) printf("encode failed %d\n", (int)cr);
-  const int smem = e::STAGES * e::STAGE_BYTES + 64;
-  CK(cudaFuncSetAttribute(e::tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const long n_ct = (c1 - c0 + e::OUTW - 1) / e::OUTW, n_rt = (r1 - r0 + e::TH - 1) / e::TH;
-  for (int grid : {148, 296}) {
-    char nm[64];
-    snprintf(nm, sizeof nm, "E tma grid%d", grid);
-    time_it(nm, [&] { e::tma_kernel<<<grid, e::THREADS, smem>>>(map, Y, n, r0, r1, c0, c1, n_ct, n_rt); });
+  {
+    dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + 15) / 16));
+    march9<16, 4, 3, 0><<<g, 256>>>(X, R, n, r0, r1, c0, c1, cbase);
+    CK(cudaDeviceSynchronize());
   }
+#define M9(ROWS, G, MINB, REC)                                                                   \
+  time_it("st9 R" #ROWS " G" #G " minB" #MINB " rec" #REC, [&] {                               \
+    dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));      \
+    march9<ROWS, G, MINB, REC><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);                     \
+  })
+  M9(16, 4, 3, 0);
+  M9(16, 2, 4, 0);
+  M9(16, 4, 4, 1);
+  M9(16, 2, 5, 1);
+  M9(32, 4, 4, 1);
+  M9(8, 2, 5, 1);
+  M9(16, 4, 5, 1);
   // plain copy for reference bandwidth
   {
     cudaEventRecord(a);
