@@ -309,6 +309,9 @@ static void ks_wait(KSync& k, unsigned long long* p, unsigned long long v) {
   k.wait_val[k.nwait] = v;
   k.nwait++;
 }
+static void ks_sig(KSync& k, unsigned long long* p) {
+  if (k.nsig < kKSync) k.sig_ptr[k.nsig++] = p;
+}
 
 static int check_err_flag(hda_ctx_t* ctx) {
   if (ctx->err_host && *(volatile int*)ctx->err_host) {
@@ -352,8 +355,16 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
       PullJob job;
       job.dst = q;
       std::vector<RunDesc> descs;
-      for (const Msg& m : t->msgs) {
-        if (m.dst != q) continue;
+      // permutation schedule: device q pulls from q+1, q+2, ... (mod P) so that at any
+      // moment every source serves one reader instead of all readers hitting src 0
+      std::vector<const Msg*> mine;
+      for (const Msg& m : t->msgs)
+        if (m.dst == q) mine.push_back(&m);
+      std::stable_sort(mine.begin(), mine.end(), [&](const Msg* a, const Msg* b) {
+        return (a->src - q + P) % P < (b->src - q + P) % P;
+      });
+      for (const Msg* mp : mine) {
+        const Msg& m = *mp;
         const TArray& a = ctx->tr->array(m.array);
         int64_t S[3];
         front_shape(a.ndim, a.shape, S);
@@ -556,7 +567,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
       for (int p : job.srcs)
         if (!same_stream(ctx, p, q)) {
           ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
-          post.sig_ptr[post.nsig++] = ctx->dev[p].sync + SW_ACK + q;
+          ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
         }
       int rc;
       cudaEvent_t a = nullptr;
@@ -677,7 +688,7 @@ static void signal_prod(hda_ctx_t* ctx, int q, unsigned long long k, KSync& ks) 
   ks.sig_val = k;
   ks.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_KERN);
   for (int r = 0; r < ctx->P; r++)
-    if (r != q && !same_stream(ctx, q, r)) ks.sig_ptr[ks.nsig++] = ctx->dev[r].sync + SW_PROD + q;
+    if (r != q && !same_stream(ctx, q, r)) ks_sig(ks, ctx->dev[r].sync + SW_PROD + q);
 }
 
 // separate wait/signal kernels, for phases that launch no kernel of their own

@@ -254,7 +254,6 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
   const int64_t rs = r0 + (int64_t)blockIdx.y * ROWS;
   const int64_t re = min(rs + (int64_t)ROWS, r1);
   T w[W][V];
-  T lft[W], rgt[W];  // left neighbour of element 0, right neighbour of element V-1
 
   auto load_row = [&](T(&r)[V], int64_t row) {
     if (live) {
@@ -275,10 +274,6 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
 
   load_row(w[0], rs - 1);
   load_row(w[1], rs);
-  if (KIND == 1) {
-    edges(w[0], rs - 1, lft[0], rgt[0]);
-    edges(w[1], rs, lft[1], rgt[1]);
-  }
   for (int64_t base = rs; base < re; base += ST_GROUP) {
 #pragma unroll
     for (int k = 0; k < ST_GROUP; k++)
@@ -298,16 +293,21 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
           o[v] = quarter<T>(((left + right) + w[k][v]) + w[k + 2][v]);
         }
       } else {
-        edges(w[k + 2], r + 1, lft[k + 2], rgt[k + 2]);
+        // recompute the row-edge shuffles of up/cur/dn for every output row: keeping
+        // them in a register window cost occupancy (tuned: 84% vs 73% of HBM)
+        T ul, ur, cl, cr, dl, dr;
+        edges(w[k], r - 1, ul, ur);
+        edges(w[k + 1], r, cl, cr);
+        edges(w[k + 2], r + 1, dl, dr);
 #pragma unroll
         for (int v = 0; v < V; v++) {
           const T* up = w[k];
           const T* cu = w[k + 1];
           const T* dn = w[k + 2];
-          const T cl = v == 0 ? lft[k + 1] : cu[v - 1], cr = v == V - 1 ? rgt[k + 1] : cu[v + 1];
-          const T ul = v == 0 ? lft[k] : up[v - 1], ur = v == V - 1 ? rgt[k] : up[v + 1];
-          const T dl = v == 0 ? lft[k + 2] : dn[v - 1], dr = v == V - 1 ? rgt[k + 2] : dn[v + 1];
-          o[v] = st9<T>(cl, cr, up[v], dn[v], ul, ur, dl, dr);
+          const T cL = v == 0 ? cl : cu[v - 1], cR = v == V - 1 ? cr : cu[v + 1];
+          const T uL = v == 0 ? ul : up[v - 1], uR = v == V - 1 ? ur : up[v + 1];
+          const T dL = v == 0 ? dl : dn[v - 1], dR = v == V - 1 ? dr : dn[v + 1];
+          o[v] = st9<T>(cL, cR, up[v], dn[v], uL, uR, dL, dR);
         }
       }
       if (live) {
@@ -326,17 +326,11 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
       w[0][v] = w[ST_GROUP][v];
       w[1][v] = w[ST_GROUP + 1][v];
     }
-    if (KIND == 1) {
-      lft[0] = lft[ST_GROUP];
-      rgt[0] = rgt[ST_GROUP];
-      lft[1] = lft[ST_GROUP + 1];
-      rgt[1] = rgt[ST_GROUP + 1];
-    }
   }
 }
 
 template <typename T, int KIND, int ROWS>
-__global__ void __launch_bounds__(ST_THREADS, (KIND == 1 && sizeof(T) == 8) ? ST_MINB - 1 : ST_MINB)
+__global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     stencil2d_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld, const __grid_constant__ Boxes2 bx,
                      const __grid_constant__ KSync ks) {
   ks_pre(ks);
@@ -427,90 +421,92 @@ cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t*
 }
 
 // =====================================================================================
-// 3-D 7-point stencil: a warp owns 32 column vectors of one (z, y) row and marches
-// in z keeping planes z-1, z, z+1 in registers; y neighbours are plain loads (their
-// rows are fetched by the neighbouring warps of the block, so they hit L1/L2).
+// 3-D 7-point stencil.  A block's 8 warps span S3_X = 1024 contiguous floats of a row
+// (4 KiB DRAM bursts; a block that spans 8 rows x 512 B plateaued at 69% of HBM),
+// each thread owns S3_R consecutive y rows (their y neighbours come from registers;
+// only rows y-1 and y+S3_R are extra, L2-resident loads) and marches S3_ZCH planes in z
+// keeping planes z-1, z, z+1 in registers.  Tuned on 1024^3 f32: 84% of HBM.
 // =====================================================================================
 
-constexpr int S3_BY = 8;   // warps per block (rows in y)
-constexpr int S3_ZCH = 16; // planes per block
+constexpr int S3_R = 2;     // y rows per thread
+constexpr int S3_ZCH = 32;  // planes per block
 
 template <typename T>
-__device__ __forceinline__ void stencil7_rows(const T* __restrict__ in, T* __restrict__ out, int64_t n1, int64_t n2,
-                                              int64_t z0, int64_t z1, int64_t x0, int64_t x1, int64_t x, int64_t y,
-                                              int lane);
-
-template <typename T>
-__global__ void __launch_bounds__(32 * S3_BY) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out,
-                                                             int64_t n1, int64_t n2, int64_t z0, int64_t z1,
-                                                             int64_t y0, int64_t y1, int64_t x0, int64_t x1,
-                                                             int64_t xbase, const __grid_constant__ KSync ks) {
+__global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n1,
+                                                         int64_t n2, int64_t z0, int64_t z1, int64_t y0, int64_t y1,
+                                                         int64_t x0, int64_t x1, int64_t xbase,
+                                                         const __grid_constant__ KSync ks) {
   ks_pre(ks);
   constexpr int V = V16<T>::n;
-  const int lane = threadIdx.x;
-  const int64_t x = xbase + ((int64_t)blockIdx.x * 32 + lane) * V;
-  const int64_t y = y0 + (int64_t)blockIdx.y * S3_BY + threadIdx.y;
-  if (y < y1) stencil7_rows<T>(in, out, n1, n2, z0, z1, x0, x1, x, y, lane);  // warp-uniform
-  ks_post(ks);
-}
-
-template <typename T>
-__device__ __forceinline__ void stencil7_rows(const T* __restrict__ in, T* __restrict__ out, int64_t n1, int64_t n2,
-                                              int64_t z0, int64_t z1, int64_t x0, int64_t x1, int64_t x, int64_t y,
-                                              int lane) {
-  constexpr int V = V16<T>::n;
+  const int lane = threadIdx.x & 31;
+  const int64_t x = xbase + ((int64_t)blockIdx.x * 256 + threadIdx.x) * V;
+  const int64_t ya = y0 + (int64_t)blockIdx.y * S3_R;
   const bool live = x < n2;
-  const int64_t zs = z0 + (int64_t)blockIdx.z * S3_ZCH;
-  const int64_t ze = min(zs + (int64_t)S3_ZCH, z1);
-  const int64_t plane = n1 * n2;
+  const int64_t zs = z0 + (int64_t)blockIdx.z * S3_ZCH, ze = min(zs + (int64_t)S3_ZCH, z1);
+  const int64_t pl = n1 * n2;
   auto ld = [&](T(&r)[V], int64_t z, int64_t yy) {
-    if (live) {
-      V16<T>::load(r, in + z * plane + yy * n2 + x);
+    if (live && yy < n1) {
+      V16<T>::load(r, in + z * pl + yy * n2 + x);
     } else {
 #pragma unroll
       for (int v = 0; v < V; v++) r[v] = T(0);
     }
   };
-  T zm[V], zc[V], zp[V], ym[V], yp[V];
-  ld(zm, zs - 1, y);
-  ld(zc, zs, y);
+  T zm[S3_R][V], zc[S3_R][V], zp[S3_R][V];
+#pragma unroll
+  for (int r = 0; r < S3_R; r++) {
+    ld(zm[r], zs - 1, ya + r);
+    ld(zc[r], zs, ya + r);
+  }
   for (int64_t z = zs; z < ze; z++) {
-    ld(zp, z + 1, y);
-    ld(ym, z, y - 1);
-    ld(yp, z, y + 1);
-    T L = __shfl_up_sync(0xffffffffu, zc[V - 1], 1);
-    T R = __shfl_down_sync(0xffffffffu, zc[0], 1);
-    const T* row = in + z * plane + y * n2 + x;
-    if (lane == 0 && live && x > 0) L = __ldg(row - 1);
-    if (lane == 31 && live && x + V < n2) R = __ldg(row + V);
-    T o[V];
+    T top[V], bot[V];
+    ld(top, z, ya - 1);
+    ld(bot, z, ya + S3_R);
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-      const T xl = v == 0 ? L : zc[v - 1];
-      const T xr = v == V - 1 ? R : zc[v + 1];
-      T s = xl + xr;
-      s = s + ym[v];
-      s = s + yp[v];
-      s = s + zm[v];
-      s = s + zp[v];
-      o[v] = s / T(6);
-    }
-    if (live) {
-      T* dst = out + z * plane + y * n2 + x;
-      if (x >= x0 && x + V <= x1) {
-        V16<T>::store(dst, o);
-      } else {
+    for (int r = 0; r < S3_R; r++) ld(zp[r], z + 1, ya + r);
 #pragma unroll
-        for (int v = 0; v < V; v++)
-          if (x + v >= x0 && x + v < x1) dst[v] = o[v];
+    for (int r = 0; r < S3_R; r++) {
+      const int64_t y = ya + r;
+      const T* c = zc[r];
+      const T* ym = r == 0 ? top : zc[r - 1];
+      const T* yp = r == S3_R - 1 ? bot : zc[r + 1];
+      T L = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
+      T R = __shfl_down_sync(0xffffffffu, c[0], 1);
+      const T* row = in + z * pl + y * n2 + x;
+      if (lane == 0 && live && x > 0 && y < y1) L = __ldg(row - 1);
+      if (lane == 31 && live && x + V < n2 && y < y1) R = __ldg(row + V);
+      T o[V];
+#pragma unroll
+      for (int v = 0; v < V; v++) {
+        const T xl = v == 0 ? L : c[v - 1];
+        const T xr = v == V - 1 ? R : c[v + 1];
+        T s = xl + xr;
+        s = s + ym[v];
+        s = s + yp[v];
+        s = s + zm[r][v];
+        s = s + zp[r][v];
+        o[v] = s / T(6);
+      }
+      if (live && y < y1) {
+        T* dst = out + z * pl + y * n2 + x;
+        if (x >= x0 && x + V <= x1) {
+          V16<T>::store(dst, o);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; v++)
+            if (x + v >= x0 && x + v < x1) dst[v] = o[v];
+        }
       }
     }
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-      zm[v] = zc[v];
-      zc[v] = zp[v];
-    }
+    for (int r = 0; r < S3_R; r++)
+#pragma unroll
+      for (int v = 0; v < V; v++) {
+        zm[r][v] = zc[r][v];
+        zc[r][v] = zp[r][v];
+      }
   }
+  ks_post(ks);
 }
 
 template <typename T>
@@ -544,11 +540,10 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
                    ((uintptr_t)out % 16) == 0;
   if (vec) {
     const int64_t xbase = lb[2] - (lb[2] % V);
-    const int64_t per = 32 * V;
-    dim3 grid((unsigned)((ub[2] - xbase + per - 1) / per), (unsigned)((ub[1] - lb[1] + S3_BY - 1) / S3_BY),
+    const int64_t per = 256 * V;
+    dim3 grid((unsigned)((ub[2] - xbase + per - 1) / per), (unsigned)((ub[1] - lb[1] + S3_R - 1) / S3_R),
               (unsigned)((ub[0] - lb[0] + S3_ZCH - 1) / S3_ZCH));
-    stencil7_kernel<T><<<grid, dim3(32, S3_BY), 0, s>>>(in, out, n1, n2, lb[0], ub[0], lb[1], ub[1], lb[2],
-                                                       ub[2], xbase, ks);
+    stencil7_kernel<T><<<grid, 256, 0, s>>>(in, out, n1, n2, lb[0], ub[0], lb[1], ub[1], lb[2], ub[2], xbase, ks);
   } else {
     dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));
     stencil7_scalar_kernel<T><<<grid, 128, 0, s>>>(in, out, n1, n2, lb[0], lb[1], ub[1], lb[2], ub[2], ks);

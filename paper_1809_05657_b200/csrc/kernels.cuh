@@ -26,7 +26,7 @@ struct RunDesc {
   int64_t chunk_bytes;  // bytes per chunk (multiple of 512)
 };
 
-constexpr int kMaxRunDescs = 24;
+constexpr int kMaxRunDescs = 8;  // per launch (kernel parameters stay small)
 struct RunBatch {
   RunDesc d[kMaxRunDescs];
   int32_t n;
@@ -53,10 +53,11 @@ struct SignalList {
 };
 
 // in-kernel cross-device ordering (sync.cuh); nwait == nsig == 0 means "none"
+constexpr int kKSync = kMaxDev;
 struct KSync {
-  unsigned long long* wait_ptr[kMaxDev];
-  unsigned long long wait_val[kMaxDev];
-  unsigned long long* sig_ptr[kMaxDev];
+  unsigned long long* wait_ptr[kKSync];
+  unsigned long long wait_val[kKSync];
+  unsigned long long* sig_ptr[kKSync];
   unsigned long long sig_val;
   unsigned int* ctr;
   int* err;

@@ -275,6 +275,33 @@ class HDArray:
         sc = (ctypes.c_double * max(len(scalars), 1))(*[float(s) for s in scalars])
         self._chk(self.L.hda_apply_abs(self.h, kernel, part, entries, n, sc, len(scalars)))
 
+    def prepare(self, kernel, part, acc, scalars=()):
+        """Marshal an hda_apply call once; the returned callable re-issues it with no
+        Python-side re-marshalling (steady-state loops)."""
+        n = len(acc)
+        entries = (hda_access_t * max(n, 1))()
+        keep = []
+        for i, (a, uses, defs) in enumerate(acc):
+            nd = len(self.shapes[a])
+            u = _tuples(uses, nd)
+            d = _tuples(defs, nd)
+            keep += [u, d]
+            entries[i].array = a
+            entries[i].n_use = len(uses)
+            entries[i].use = ctypes.cast(u, ctypes.POINTER(ctypes.c_int32))
+            entries[i].n_def = len(defs)
+            entries[i].def_ = ctypes.cast(d, ctypes.POINTER(ctypes.c_int32))
+        sc = (ctypes.c_double * max(len(scalars), 1))(*[float(s) for s in scalars])
+        fn, h, ns = self.L.hda_apply, self.h, len(scalars)
+
+        def run():
+            rc = fn(h, kernel, part, entries, n, sc, ns)
+            if rc:
+                self._chk(rc)
+
+        run._keep = (entries, keep, sc)
+        return run
+
     def sync(self):
         self._chk(self.L.hda_sync(self.h))
 

@@ -51,7 +51,7 @@ static void all_to_all(int G, size_t bytes) {
     cudaEventCreate(&e1[g]);
   }
   const size_t n = bytes / 16;
-  for (int mode = 0; mode < 3; mode++) {
+  for (int mode = 0; mode < 5; mode++) {
     float best = 1e30f;
     for (int rep = 0; rep < 4; rep++) {
       for (int g = 0; g < G; g++) {
@@ -69,6 +69,10 @@ static void all_to_all(int G, size_t bytes) {
           }
           if (mode == 2)
             copy_kernel<4><<<148 * 8, 256, 0, s>>>((const uint4*)src[h], (uint4*)((char*)dst[g] + h * bytes), n);
+          else if (mode == 3)  // CE push: g writes its block into peer h
+            CK(cudaMemcpyPeerAsync((char*)dst[h] + g * bytes, h, src[g], g, bytes, s));
+          else if (mode == 4)  // SM push
+            copy_kernel<4><<<148 * 8, 256, 0, s>>>((const uint4*)src[g], (uint4*)((char*)dst[h] + g * bytes), n);
           else
             CK(cudaMemcpyPeerAsync((char*)dst[g] + h * bytes, g, src[h], h, bytes, s));
         }
@@ -93,7 +97,8 @@ static void all_to_all(int G, size_t bytes) {
       }
       best = worst < best ? worst : best;
     }
-    const char* nm[3] = {"CE one stream", "CE stream per peer", "SM pull x4"};
+    const char* nm[5] = {"CE pull one stream", "CE pull stream/peer", "SM pull x4", "CE push one stream",
+                         "SM push x4"};
     printf("all-to-all G=%d %-22s %8.3f ms  per-GPU in %7.1f GB/s\n", G, nm[mode], best,
            (G - 1) * bytes / (best * 1e-3) / 1e9);
   }
