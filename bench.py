@@ -374,6 +374,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--transport", type=int, default=2, help="0 fused SM pull, 1 staged, 2 auto (default)")
     ap.add_argument("--no-overlap", action="store_true")
+    ap.add_argument("--trace", type=int, default=0, help="trace N steps after the timed region")
     args = ap.parse_args()
     defaults = {"jacobi2d": (1000, 20), "stencil9": (200, 10), "stencil7": (100, 5), "repartition": (40, 4),
                 "gemm": (20, 3)}[args.workload]
@@ -529,6 +530,26 @@ def main():
             roof["traffic"] = json.load(open(tp)).get(f"{args.workload}_n{wl.n}_P{ws}")
         except Exception:
             pass
+
+    # N=1 stencil steps are exactly one kernel launch: take the roofline from the timed
+    # region itself (CUDA events on the kernel's stream), not from the bracketing pass
+    if ws == 1 and isinstance(wl, Stencil) and launches == args.steps:
+        roof["avg_launch_ms_bracketed"] = roof["avg_launch_ms"]
+        roof["avg_launch_ms"] = ms / args.steps
+        roof["achieved"] = wl.alg_per_launch / (roof["avg_launch_ms"] * 1e-3) / 1e9
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["timing"] = "timed region (one launch per step)"
+    if args.trace:
+        barrier()
+        h.set_trace(True)
+        for _ in range(args.trace):
+            wl.step()
+        barrier()
+        tr = h.trace()
+        h.set_trace(False)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"trace_{args.workload}_n{ws}_r{rank}.json"), "w") as f:
+            json.dump(tr.tolist(), f)
 
     par = wl.parity()
 

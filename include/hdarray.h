@@ -279,6 +279,13 @@ int hda_set_kernel_timing(hda_ctx_t* ctx, int32_t enabled);
 int hda_kernel_time(hda_ctx_t* ctx, int32_t kernel, double* total_ms, int64_t* launches);
 /* exchange timing (same mechanism, brackets the pull / pack-copy-unpack work) */
 int hda_exchange_time(hda_ctx_t* ctx, double* total_ms, int64_t* n);
+/* tracing (SURVEY §5 "CUDA events per device per phase"): while enabled, every
+ * exchange and kernel launch of every call is bracketed by CUDA events; hda_trace
+ * returns rows {call epoch, device, phase, start_us, end_us} (phase 0 exchange,
+ * 1 kernel, 2 interior part, 3 dependent part), times relative to enabling; blocks.
+ * Events are recorded only on this process's devices and streams. */
+int hda_set_trace(hda_ctx_t* ctx, int32_t enabled);
+int hda_trace(hda_ctx_t* ctx, double* out, int32_t cap, int32_t* n_out);
 /* cudaStream_t of a local device, for callers that record their own events */
 int hda_stream(hda_ctx_t* ctx, int32_t dev, void** stream);
 

@@ -73,6 +73,8 @@ struct TimedEv {
   int kind;  // kernel id, or -100 for exchange
   cudaEvent_t a, b;
   int count;  // 1 for the first launch of a call, 0 for its continuation launches
+  unsigned long long epoch;
+  int dev, phase;  // phase: 0 exchange, 1 kernel (whole), 2 interior, 3 dependent
 };
 
 struct PullJob {
@@ -130,7 +132,10 @@ struct hda_ctx {
   std::vector<size_t> send_cap, recv_cap;
   std::unordered_map<uint64_t, ExecPlan> exec;
   int transport = HDA_XPORT_AUTO;
-  bool cache_on = true, ktiming = false, overlap = true;
+  bool cache_on = true, ktiming = false, overlap = true, tracing = false;
+  std::vector<TimedEv> trace;  // kept (not drained) while tracing
+  cudaEvent_t trace_ref = nullptr;
+  int cur_dev = 0, cur_phase = 1;
   std::vector<char> pulled_on_comm;  // [P] this call's pull for device q ran on the comm stream
   std::vector<const PullJob*> cur_pull;
   std::vector<TimedEv> tev;
@@ -515,7 +520,7 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
 
 static int timed_begin(hda_ctx_t* ctx, cudaStream_t st, cudaEvent_t* a) {
   *a = nullptr;
-  if (!ctx->ktiming) return HDA_OK;
+  if (!ctx->ktiming && !ctx->tracing) return HDA_OK;
   *a = get_event(ctx);
   CK(cudaEventRecord(*a, st));
   return HDA_OK;
@@ -524,7 +529,12 @@ static int timed_end(hda_ctx_t* ctx, cudaStream_t st, int kind, cudaEvent_t a, i
   if (!a) return HDA_OK;
   cudaEvent_t b = get_event(ctx);
   CK(cudaEventRecord(b, st));
-  ctx->tev.push_back(TimedEv{kind, a, b, count});
+  TimedEv e{kind, a, b, count, ctx->epoch, ctx->cur_dev, kind == -100 ? 0 : ctx->cur_phase};
+  if (ctx->tracing) {
+    ctx->trace.push_back(e);
+  } else {
+    ctx->tev.push_back(e);
+  }
   return HDA_OK;
 }
 
@@ -608,6 +618,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
         CK(launch_copy_runs(job.batches[i], ks, st));
         count_launch(ctx);
       }
+      ctx->cur_dev = q;
       if ((rc = timed_end(ctx, st, -100, a))) return rc;
       if (comm) CK(cudaEventRecord(g.ev_pull, g.comm));
       for (auto& pr : job.pend) ctx->pend[pr.first][pr.second][q] = k;
@@ -951,6 +962,8 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
           cudaEvent_t a;
           if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
           if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, true, !has_d), &job.interior))) return rc;
+          ctx->cur_dev = q;
+          ctx->cur_phase = 2;
           if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
         }
         if (has_d) {
@@ -959,6 +972,8 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
           cudaEvent_t a;
           if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
           if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, !has_i, true), &job.dependent))) return rc;
+          ctx->cur_dev = q;
+          ctx->cur_phase = 3;
           if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
         }
         if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
@@ -967,6 +982,8 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         cudaEvent_t a;
         if ((rc = timed_begin(ctx, stream_of(ctx, q), &a))) return rc;
         if ((rc = run_kernel(ctx, t, q, scalars, ks))) return rc;
+        ctx->cur_dev = q;
+        ctx->cur_phase = 1;
         if ((rc = timed_end(ctx, stream_of(ctx, q), kernel, a))) return rc;
       } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
         return rc;
@@ -1557,6 +1574,47 @@ int hda_exchange_time(hda_ctx_t* ctx, double* total_ms, int64_t* n) {
   if (rc) return rc;
   *total_ms = ctx->xtime_ms;
   *n = ctx->xcount;
+  return HDA_OK;
+}
+
+int hda_set_trace(hda_ctx_t* ctx, int32_t enabled) {
+  GUARD();
+  if (ctx->plan_only) return HDA_OK;
+  DevGuard g(true);
+  if (enabled && !ctx->tracing) {
+    for (auto& e : ctx->trace) {
+      ctx->ev_pool.push_back(e.a);
+      ctx->ev_pool.push_back(e.b);
+    }
+    ctx->trace.clear();
+    if (!ctx->trace_ref) CK(cudaEventCreate(&ctx->trace_ref));
+    const int d0 = ctx->spmd ? ctx->rank : 0;
+    CK(cudaSetDevice(ordinal_of(ctx, d0)));
+    CK(cudaEventRecord(ctx->trace_ref, stream_of(ctx, d0)));
+  }
+  ctx->tracing = enabled != 0;
+  return HDA_OK;
+}
+
+int hda_trace(hda_ctx_t* ctx, double* out, int32_t cap, int32_t* n_out) {
+  GUARD();
+  if (!n_out) return fail(ctx, HDA_EINVAL, "null n_out");
+  *n_out = (int32_t)ctx->trace.size();
+  if (!out || ctx->trace.empty()) return HDA_OK;
+  DevGuard g(true);
+  int rc = sync_all(ctx);
+  if (rc) return rc;
+  for (int32_t i = 0; i < cap && i < *n_out; i++) {
+    const TimedEv& e = ctx->trace[i];
+    float t0 = 0, t1 = 0;
+    CK(cudaEventElapsedTime(&t0, ctx->trace_ref, e.a));
+    CK(cudaEventElapsedTime(&t1, ctx->trace_ref, e.b));
+    out[5 * i + 0] = (double)e.epoch;
+    out[5 * i + 1] = e.dev;
+    out[5 * i + 2] = e.phase;
+    out[5 * i + 3] = t0 * 1e3;
+    out[5 * i + 4] = t1 * 1e3;
+  }
   return HDA_OK;
 }
 

@@ -54,7 +54,7 @@ EXPORTS = [
     "hda_spmd_import", "hda_create", "hda_create_ext", "hda_free", "hda_device_ptr", "hda_partition",
     "hda_partition_manual", "hda_partition_region", "hda_apply", "hda_apply_abs", "hda_trapezoid", "hda_sync", "hda_write", "hda_read", "hda_reduce",
     "hda_set_transport", "hda_set_overlap", "hda_set_plan_cache", "hda_set_kernel_timing", "hda_kernel_time", "hda_exchange_time",
-    "hda_stream", "hda_last_plan", "hda_owner_map", "hda_read_replica", "hda_stats", "hda_reset_stats",
+    "hda_stream", "hda_set_trace", "hda_trace", "hda_last_plan", "hda_owner_map", "hda_read_replica", "hda_stats", "hda_reset_stats",
     "hda_last_error", "hda_version",
 ]
 
@@ -100,6 +100,8 @@ def lib():
             "hda_kernel_time": [vp, i32, P(ctypes.c_double), P(i64)],
             "hda_exchange_time": [vp, P(ctypes.c_double), P(i64)],
             "hda_stream": [vp, i32, P(vp)],
+            "hda_set_trace": [vp, i32],
+            "hda_trace": [vp, P(ctypes.c_double), i32, P(i32)],
             "hda_last_plan": [vp, P(hda_msg_t), i32, P(i32)],
             "hda_owner_map": [vp, i32, vp],
             "hda_read_replica": [vp, i32, i32, vp],
@@ -355,6 +357,18 @@ class HDArray:
         n = ctypes.c_int64()
         self._chk(self.L.hda_exchange_time(self.h, ctypes.byref(ms), ctypes.byref(n)))
         return ms.value, n.value
+
+    def set_trace(self, on):
+        self._chk(self.L.hda_set_trace(self.h, 1 if on else 0))
+
+    def trace(self):
+        """rows (epoch, device, phase, start_us, end_us); phase 0 exchange, 1 kernel,
+        2 interior, 3 dependent."""
+        n = ctypes.c_int32()
+        self._chk(self.L.hda_trace(self.h, None, 0, ctypes.byref(n)))
+        out = (ctypes.c_double * max(5 * n.value, 5))()
+        self._chk(self.L.hda_trace(self.h, out, n.value, ctypes.byref(n)))
+        return np.array(out[:5 * n.value]).reshape(-1, 5)
 
     def stream(self, dev):
         s = ctypes.c_void_p()

@@ -64,3 +64,30 @@ def test_plan_only_context_and_errors():
     with pytest.raises(H.HDAError) as e:
         h.stream(0)
     h.close()
+
+
+def test_prepared_call_equals_apply():
+    import paper_1809_05657_b200 as H
+    J = [(0, -1), (0, 1), (-1, 0), (1, 0)]
+    plans = []
+    for prepared in (False, True):
+        h = H.HDArray(n_gpus=0, n_devices=3)
+        A, B = h.create(H.F64, (20, 16)), h.create(H.F64, (20, 16))
+        data = h.partition(H.ROW, (20, 16))
+        work = h.partition(H.ROW, (20, 16), (1, 1), (19, 15))
+        h.write(A, data, None)
+        h.write(B, data, None)
+        fwd = [(A, [], [(0, 0)]), (B, J, [])]
+        bwd = [(B, [], [(0, 0)]), (A, J, [])]
+        if prepared:
+            calls = [h.prepare(H.K_JACOBI5, work, fwd), h.prepare(H.K_JACOBI5, work, bwd)]
+        seq = []
+        for s in range(6):
+            if prepared:
+                calls[s % 2]()
+            else:
+                h.apply(H.K_JACOBI5, work, fwd if s % 2 == 0 else bwd)
+            seq.append(h.last_plan())
+        plans.append(seq)
+        h.close()
+    assert plans[0] == plans[1] and any(plans[0])
