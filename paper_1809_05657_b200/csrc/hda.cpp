@@ -1034,7 +1034,11 @@ static int setup_gpu_common(hda_ctx_t* ctx) {
   for (auto& g : ctx->gpus) {
     CK(cudaSetDevice(g.ordinal));
     CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&g.comm, cudaStreamNonBlocking));
+    // halo pulls get the higher priority: their CTAs are scheduled ahead of the
+    // interior kernel's as SM resources free up
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&g.comm, cudaStreamNonBlocking, hi));
     CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g.ev_pull, cudaEventDisableTiming));
   }

@@ -213,6 +213,18 @@ struct V16<float> {
 // 4-row load groups, >= 4 blocks/SM -> 6.24 TB/s = 95% of the measured copy peak
 // (128 threads x 32 rows x 8-row groups at 113 registers reached only 4.99 TB/s:
 // too few warps in flight).
+static int sm_count_dev() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!n[dev]) {
+    cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (n[dev] <= 0) n[dev] = 148;
+  }
+  return n[dev];
+}
+
 constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
 constexpr int ST_ROWS = 16;      // rows per block
@@ -239,20 +251,22 @@ __device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
 // an overlapped halo exchange run as ONE launch
 struct Boxes2 {
   int64_t r0[8], r1[8], c0[8], c1[8], cbase[8];
+  int64_t rpb[8];  // rows per block (each block marches a contiguous row range)
   int32_t gx[8], gy[8];
   int32_t n;
 };
 
 template <typename T, int KIND, int ROWS>
 __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
-                                               int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase) {
+                                               int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase,
+                                               int64_t rpb) {
   constexpr int V = V16<T>::n;
   constexpr int W = ST_GROUP + 2;
   const int lane = threadIdx.x & 31;
   const int64_t col = cbase + ((int64_t)blockIdx.x * ST_THREADS + threadIdx.x) * V;
   const bool live = col < ld;
-  const int64_t rs = r0 + (int64_t)blockIdx.y * ROWS;
-  const int64_t re = min(rs + (int64_t)ROWS, r1);
+  const int64_t rs = r0 + (int64_t)blockIdx.y * rpb;
+  const int64_t re = min(rs + rpb, r1);
   T w[W][V];
 
   auto load_row = [&](T(&r)[V], int64_t row) {
@@ -336,7 +350,7 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
   ks_pre(ks);
   const int b = blockIdx.z;
   if ((int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b])  // block-uniform
-    stencil2d_body<T, KIND, ROWS>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b]);
+    stencil2d_body<T, KIND, ROWS>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b], bx.rpb[b]);
   ks_post(ks);
 }
 
@@ -382,7 +396,22 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       bx.cbase[k] = c0 - (c0 % V);
       const int64_t per_block = (int64_t)ST_THREADS * V;
       bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
-      bx.gy[k] = (int)((r1 - r0 + ROWS - 1) / ROWS);
+    }
+    // One wave: 148 SMs x ST_MINB blocks in total, each block marching a contiguous
+    // row range (2 halo rows per block, no tail wave) and leaving register headroom
+    // on every SM for an overlapped halo pull.
+    int64_t strips = 0;
+    for (int k = 0; k < bx.n; k++) strips += bx.gx[k];
+    const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
+    for (int k = 0; k < bx.n; k++) {
+      const int64_t rows = bx.r1[k] - bx.r0[k];
+      int64_t gyk = std::max<int64_t>(1, wave / std::max<int64_t>(strips, 1));
+      // narrow boxes (column strips of a BLOCK halo) have one live thread per block:
+      // split their rows as finely as possible instead
+      if (bx.c1[k] - bx.c0[k] <= 64) gyk = rows;
+      gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
+      bx.rpb[k] = (rows + gyk - 1) / gyk;
+      bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
       gx = std::max(gx, bx.gx[k]);
       gy = std::max(gy, bx.gy[k]);
     }
