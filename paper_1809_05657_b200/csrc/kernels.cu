@@ -397,19 +397,26 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       const int64_t per_block = (int64_t)ST_THREADS * V;
       bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
     }
-    // One wave: 148 SMs x ST_MINB blocks in total, each block marching a contiguous
-    // row range (2 halo rows per block, no tail wave) and leaving register headroom
-    // on every SM for an overlapped halo pull.
-    int64_t strips = 0;
-    for (int k = 0; k < bx.n; k++) strips += bx.gx[k];
+    // Large boxes: 16-row tiles, many waves (94% of HBM at 8190 rows).  Boxes that
+    // would take fewer than ~8 waves (a GPU's share at N >= 4) instead get one wave of
+    // 148 x ST_MINB blocks marching contiguous row ranges: no tail wave, 2 halo rows
+    // per block, and register headroom on every SM for an overlapped halo pull.
+    // Narrow boxes (column strips of a BLOCK halo: one live thread per block) keep
+    // 16-row tiles.
+    int64_t strips = 0, tiles16 = 0;
+    for (int k = 0; k < bx.n; k++) {
+      strips += bx.gx[k];
+      tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
+    }
     const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
+    const bool one_wave = tiles16 < 8 * wave;
     for (int k = 0; k < bx.n; k++) {
       const int64_t rows = bx.r1[k] - bx.r0[k];
-      int64_t gyk = std::max<int64_t>(1, wave / std::max<int64_t>(strips, 1));
-      // narrow boxes (column strips of a BLOCK halo) have one live thread per block:
-      // split their rows as finely as possible instead
-      if (bx.c1[k] - bx.c0[k] <= 64) gyk = rows;
-      gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
+      int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
+      if (one_wave && bx.c1[k] - bx.c0[k] > 64) {
+        gyk = std::max<int64_t>(1, wave / std::max<int64_t>(strips, 1));
+        gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
+      }
       bx.rpb[k] = (rows + gyk - 1) / gyk;
       bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
       gx = std::max(gx, bx.gx[k]);

@@ -49,7 +49,11 @@ __device__ __forceinline__ void ks_post(const KSync& s) {
     const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
     if (atomicAdd(s.ctr, 1u) == total - 1) {
       *s.ctr = 0;  // stream-ordered reuse by the next kernel of this purpose
-      __threadfence_system();
+      // every block fenced its writes to this GPU's memory at gpu scope before the
+      // counter; this GPU's L2 is the coherence point peers read through, so a
+      // gpu-scope fence plus system-scope release stores suffice (a fence.sc.sys here
+      // cost ~10 us per signalling launch)
+      __threadfence();
       for (int i = 0; i < s.nsig; i++) ks_st_release(s.sig_ptr[i], s.sig_val);
     }
   }
