@@ -27,6 +27,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -42,6 +43,7 @@ using namespace hda;
 namespace {
 
 constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_CTR_PULL = 192, SW_CTR_KERN = 193;
+constexpr int SW_PULLDONE = 194;  // local: epoch of the last completed overlapped pull
 constexpr int SW_RED = 256, SW_REDSIG = 320;  // reduce partials [P] and their epochs [P]
 constexpr int SW_SCRATCH = 384;               // kReduceBlocks partials
 constexpr int SW_WORDS = SW_SCRATCH + kReduceBlocks;
@@ -293,8 +295,17 @@ static void wl_add(WaitList& w, unsigned long long* p, unsigned long long v) {
   w.n++;
 }
 
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
 static KSync ks_empty(hda_ctx_t* ctx) {
+  // signals are relaxed system-scope stores issued after a gpu-scope fence (sync.cuh);
+  // HDA_SIG_RELEASE=1 switches to st.release.sys (measured ~4 us slower per launch)
+  static const int relaxed = env_int("HDA_SIG_RELEASE", 0) ? 0 : 1;
   KSync k;
+  k.relaxed = relaxed;
   k.nwait = 0;
   k.nsig = 0;
   k.sig_val = 0;
@@ -579,6 +590,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
           ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
           ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
         }
+      if (comm) ks_sig(post, ctx->dev[q].sync + SW_PULLDONE);  // gates the dependent strips
       int rc;
       cudaEvent_t a = nullptr;
       const size_t nb = job.batches.size();
@@ -952,12 +964,46 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
         if ((rc = sync_only(ctx, q, post))) return rc;
       } else if (kern && ctx->pulled_on_comm[q]) {
-        // interior boxes while the pull is in flight, dependent boxes after it (one
-        // launch each for the 2-D stencils)
+        // interior boxes while the pull is in flight, dependent boxes after it
         const PullJob& job = *ctx->cur_pull[q];
         Gpu& g = ctx->gpus[ctx->dev[q].gpu];
         bool joined = false;
         const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
+        const bool stencil2d = kernel == KN_JACOBI5 || kernel == KN_STENCIL9;
+        if (stencil2d && job.interior.size() + job.dependent.size() <= 8) {
+          // ONE launch: interior blocks first; the dependent strips' blocks (scheduled
+          // last) wait in-kernel for the pull's local release word, then read the halo
+          // with L1-bypassing loads.  The one-wave grid leaves every SM room for the
+          // pull's CTAs, so the wait cannot starve the pull.
+          const CallInfo& ci = *t->info;
+          const TArray& a0 = ctx->tr->array(ci.param_array[0]);
+          int64_t S[3];
+          front_shape(a0.ndim, a0.shape, S);
+          std::vector<Box> fb;
+          for (const Box& b : job.interior) fb.push_back(front_box(a0.ndim, b));
+          for (const Box& b : job.dependent) fb.push_back(front_box(a0.ndim, b));
+          const int64_t* lbs[8];
+          const int64_t* ubs[8];
+          for (size_t i = 0; i < fb.size(); i++) {
+            lbs[i] = fb[i].lb;
+            ubs[i] = fb[i].ub;
+          }
+          auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
+          cudaEvent_t a;
+          if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+          const unsigned long long* gw = ctx->dev[q].sync + SW_PULLDONE;
+          const int nfb = (int)fb.size(), ni = (int)job.interior.size();
+          if (kernel == KN_JACOBI5)
+            CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, lbs, ubs, nfb, ks, g.stream, gw, k, ni));
+          else
+            CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, lbs, ubs, nfb, ks, g.stream, gw, k, ni));
+          count_launch(ctx);
+          ctx->cur_dev = q;
+          ctx->cur_phase = 1;
+          if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
+          CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));  // keep later stream work ordered
+          joined = true;
+        } else {
         if (has_i) {
           cudaEvent_t a;
           if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
@@ -975,6 +1021,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
           ctx->cur_dev = q;
           ctx->cur_phase = 3;
           if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
+        }
         }
         if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
         ctx->pulled_on_comm[q] = 0;

@@ -190,6 +190,12 @@ struct V16<double> {
     r[0] = v.x;
     r[1] = v.y;
   }
+  // coherent (L1-bypassing) load: data another kernel is writing during this one
+  __device__ static void load_cg(double (&r)[2], const double* p) {
+    double2 v = __ldcg(reinterpret_cast<const double2*>(p));
+    r[0] = v.x;
+    r[1] = v.y;
+  }
   __device__ static void store(double* p, const double (&r)[2]) {
     *reinterpret_cast<double2*>(p) = make_double2(r[0], r[1]);
   }
@@ -199,6 +205,13 @@ struct V16<float> {
   static constexpr int n = 4;
   __device__ static void load(float (&r)[4], const float* p) {
     float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    r[0] = v.x;
+    r[1] = v.y;
+    r[2] = v.z;
+    r[3] = v.w;
+  }
+  __device__ static void load_cg(float (&r)[4], const float* p) {
+    float4 v = __ldcg(reinterpret_cast<const float4*>(p));
     r[0] = v.x;
     r[1] = v.y;
     r[2] = v.z;
@@ -256,7 +269,7 @@ struct Boxes2 {
   int32_t n;
 };
 
-template <typename T, int KIND, int ROWS>
+template <typename T, int KIND, int ROWS, bool CG>
 __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
                                                int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase,
                                                int64_t rpb) {
@@ -271,7 +284,10 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
 
   auto load_row = [&](T(&r)[V], int64_t row) {
     if (live) {
-      V16<T>::load(r, in + row * ld + col);
+      if (CG)
+        V16<T>::load_cg(r, in + row * ld + col);
+      else
+        V16<T>::load(r, in + row * ld + col);
     } else {
 #pragma unroll
       for (int v = 0; v < V; v++) r[v] = T(0);
@@ -282,8 +298,8 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
     R = __shfl_down_sync(0xffffffffu, r[0], 1);
     // the neighbour of column 0 / ld-1 is never used (work boxes keep a 1-cell ring),
     // and loading it would step outside the replica for the first / last row
-    if (lane == 0 && live && col > 0) L = __ldg(in + row * ld + col - 1);
-    if (lane == 31 && live && col + V < ld) R = __ldg(in + row * ld + col + V);
+    if (lane == 0 && live && col > 0) L = CG ? __ldcg(in + row * ld + col - 1) : __ldg(in + row * ld + col - 1);
+    if (lane == 31 && live && col + V < ld) R = CG ? __ldcg(in + row * ld + col + V) : __ldg(in + row * ld + col + V);
   };
 
   load_row(w[0], rs - 1);
@@ -343,14 +359,42 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
   }
 }
 
+// gate: boxes with index >= first_gated read cells an overlapped halo pull is writing
+// concurrently; their blocks (scheduled last) wait until *gate >= gate_val (released by
+// the pull kernel's last CTA) and read with L1-bypassing loads.
+struct Gate {
+  const unsigned long long* word;
+  unsigned long long val;
+  int32_t first_gated;
+};
+
 template <typename T, int KIND, int ROWS>
 __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     stencil2d_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld, const __grid_constant__ Boxes2 bx,
-                     const __grid_constant__ KSync ks) {
+                     const __grid_constant__ KSync ks, const Gate gate) {
   ks_pre(ks);
   const int b = blockIdx.z;
-  if ((int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b])  // block-uniform
-    stencil2d_body<T, KIND, ROWS>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b], bx.rpb[b]);
+  const bool inside = (int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b];  // block-uniform
+  if (b >= gate.first_gated) {
+    if (threadIdx.x == 0 && inside) {
+      const unsigned long long t0 = ks_timer();
+      while (ks_ld_acquire(gate.word) < gate.val) {
+        __nanosleep(64);
+        if ((long long)(ks_timer() - t0) > ks.timeout_ns) {
+          *reinterpret_cast<volatile int*>(ks.err) = -7;
+          __threadfence_system();
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    if (inside)
+      stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                          bx.rpb[b]);
+  } else if (inside) {
+    stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                         bx.rpb[b]);
+  }
   ks_post(ks);
 }
 
@@ -375,7 +419,9 @@ __global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict_
 
 template <typename T, int KIND>
 static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* const* lbs,
-                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
+                                      const unsigned long long* gate_word, unsigned long long gate_val,
+                                      int first_gated) {
   const int64_t ld = shape[2];
   constexpr int V = V16<T>::n;
   const bool vec = (ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
@@ -385,9 +431,11 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     Boxes2 bx;
     bx.n = 0;
     int gx = 1, gy = 1;
+    int gated_from = 8;
     for (int i = 0; i < nb; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
       if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
+      if (i >= first_gated && gated_from == 8) gated_from = bx.n;
       const int k = bx.n++;
       bx.r0[k] = r0;
       bx.r1[k] = r1;
@@ -426,7 +474,8 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       bx.n = 1;
       bx.gx[0] = bx.gy[0] = 0;
     }
-    stencil2d_kernel<T, KIND, ROWS><<<dim3(gx, gy, bx.n), ST_THREADS, 0, s>>>(in, out, ld, bx, ks);
+    Gate gate{gate_word, gate_val, gate_word ? gated_from : 8};
+    stencil2d_kernel<T, KIND, ROWS><<<dim3(gx, gy, bx.n), ST_THREADS, 0, s>>>(in, out, ld, bx, ks, gate);
   } else {
     for (int i = 0; i < nb; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
@@ -443,17 +492,23 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
 }
 
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
-                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
+                           const unsigned long long* gate_word, unsigned long long gate_val, int first_gated) {
   if (dtype == 0)
-    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
-  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
+    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s, gate_word,
+                                         gate_val, first_gated);
+  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s, gate_word, gate_val,
+                                      first_gated);
 }
 
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
-                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
+                            const unsigned long long* gate_word, unsigned long long gate_val, int first_gated) {
   if (dtype == 0)
-    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
-  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
+    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s, gate_word,
+                                         gate_val, first_gated);
+  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s, gate_word, gate_val,
+                                      first_gated);
 }
 
 // =====================================================================================

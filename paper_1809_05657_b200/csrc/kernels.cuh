@@ -63,6 +63,7 @@ struct KSync {
   int* err;
   long long timeout_ns;
   int32_t nwait, nsig;
+  int32_t relaxed;  // experiment: signal with st.relaxed.sys after a gpu-scope fence
 };
 
 struct BoxList {  // boxes in element coordinates of a 3-D padded shape
@@ -77,12 +78,16 @@ cudaError_t launch_signal(const SignalList& l, cudaStream_t s);
 
 // user kernels over the work box [lb, ub) of one device's replica (padded 3-D shape)
 // 2-D stencils over nb (<= 8) boxes in ONE launch (lbs[i], ubs[i] front-padded 3-D)
+// gate_word != NULL: boxes [first_gated, nb) wait for *gate_word >= gate_val (an
+// overlapped halo pull) inside the same launch
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
                            const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
-                           cudaStream_t s);
+                           cudaStream_t s, const unsigned long long* gate_word = nullptr,
+                           unsigned long long gate_val = 0, int first_gated = 8);
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
-                            cudaStream_t s);
+                            cudaStream_t s, const unsigned long long* gate_word = nullptr,
+                            unsigned long long gate_val = 0, int first_gated = 8);
 cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb,

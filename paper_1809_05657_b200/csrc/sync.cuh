@@ -49,12 +49,18 @@ __device__ __forceinline__ void ks_post(const KSync& s) {
     const unsigned int total = gridDim.x * gridDim.y * gridDim.z;
     if (atomicAdd(s.ctr, 1u) == total - 1) {
       *s.ctr = 0;  // stream-ordered reuse by the next kernel of this purpose
-      // every block fenced its writes to this GPU's memory at gpu scope before the
-      // counter; this GPU's L2 is the coherence point peers read through, so a
-      // gpu-scope fence plus system-scope release stores suffice (a fence.sc.sys here
-      // cost ~10 us per signalling launch)
+      // Every block fenced at gpu scope before the counter, so all of this kernel's
+      // writes to this GPU's memory have reached its L2 — the point peers read this
+      // memory through — and all of its loads (pulls) have returned.  A relaxed
+      // system-scope store of the flag is then enough; st.release.sys costs ~4 us per
+      // signalling launch (measured: N=4 Jacobi 1068 -> 1159 GPoints/s).
       __threadfence();
-      for (int i = 0; i < s.nsig; i++) ks_st_release(s.sig_ptr[i], s.sig_val);
+      if (s.relaxed) {
+        for (int i = 0; i < s.nsig; i++)
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(s.sig_ptr[i]), "l"(s.sig_val) : "memory");
+      } else {
+        for (int i = 0; i < s.nsig; i++) ks_st_release(s.sig_ptr[i], s.sig_val);
+      }
     }
   }
 }
