@@ -140,6 +140,7 @@ struct hda_ctx {
   int cur_dev = 0, cur_phase = 1;
   std::vector<char> pulled_on_comm;  // [P] this call's pull for device q ran on the comm stream
   std::vector<const PullJob*> cur_pull;
+  std::vector<const PullJob*> halo_job;  // [P] pull deferred into the fused halo-stencil launch
   std::vector<TimedEv> tev;
   std::vector<cudaEvent_t> ev_pool;
   double ktime_ms[KN_COUNT] = {};
@@ -549,7 +550,8 @@ static int timed_end(hda_ctx_t* ctx, cudaStream_t st, int kind, cudaEvent_t a, i
   return HDA_OK;
 }
 
-static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k, bool overlap_kernel) {
+static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k, bool overlap_kernel,
+                       bool halo_kernel) {
   if (t->msgs.empty()) return HDA_OK;
   ExecPlan* ep;
   ExecPlan scratch;
@@ -573,6 +575,13 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
       const int q = job.dst;
       CK(cudaSetDevice(ordinal_of(ctx, q)));
       Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+      // 2-D stencil with a cross-GPU halo: the pull runs inside the stencil launch
+      if (ctx->overlap && halo_kernel && job.cross && job.split && job.ce.empty() && job.batches.size() == 1 &&
+          job.srcs.size() <= 8 && job.interior.size() + job.dependent.size() <= 8) {
+        ctx->halo_job[q] = &job;
+        for (auto& pr : job.pend) ctx->pend[pr.first][pr.second][q] = k;
+        continue;
+      }
       const bool comm = ctx->overlap && job.cross && job.split && overlap_kernel;
       cudaStream_t st = comm ? g.comm : g.stream;
       if (comm) {  // the pull may start as soon as everything issued before this call is done
@@ -906,7 +915,8 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     DevGuard g(true);
     const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
                                 kernel == KN_SCALE || kernel == KN_COPY;
-    if ((rc = do_exchange(ctx, t, k, overlap_kernel))) return rc;
+    const bool halo_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9;
+    if ((rc = do_exchange(ctx, t, k, overlap_kernel, halo_kernel))) return rc;
     const TPart& pt = ctx->tr->part(part);
     for (int q = 0; q < ctx->P; q++) {
       if (!ctx->dev[q].local) continue;
@@ -963,6 +973,46 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         }
         if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
         if ((rc = sync_only(ctx, q, post))) return rc;
+      } else if (kern && ctx->halo_job[q]) {
+        // fused halo-exchange stencil: pull + interior + dependent strips, one launch
+        const PullJob& job = *ctx->halo_job[q];
+        ctx->halo_job[q] = nullptr;
+        const CallInfo& ci = *t->info;
+        const TArray& a0 = ctx->tr->array(ci.param_array[0]);
+        int64_t S[3];
+        front_shape(a0.ndim, a0.shape, S);
+        std::vector<Box> fb;
+        for (const Box& b : job.interior) fb.push_back(front_box(a0.ndim, b));
+        for (const Box& b : job.dependent) fb.push_back(front_box(a0.ndim, b));
+        const int64_t* lbs[8];
+        const int64_t* ubs[8];
+        for (size_t i = 0; i < fb.size(); i++) {
+          lbs[i] = fb[i].lb;
+          ubs[i] = fb[i].ub;
+        }
+        HaloPull hp;
+        std::memset(&hp, 0, sizeof hp);
+        for (int p : job.srcs)
+          if (!same_stream(ctx, p, q)) {
+            if (ctx->last_prod[p]) {
+              hp.wait_ptr[hp.nwait] = ctx->dev[q].sync + SW_PROD + p;
+              hp.wait_val[hp.nwait++] = ctx->last_prod[p];
+            }
+            hp.ack_ptr[hp.nack++] = ctx->dev[p].sync + SW_ACK + q;
+          }
+        hp.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
+        hp.done_word = ctx->dev[q].sync + SW_PULLDONE;
+        hp.epoch = k;
+        auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
+        cudaStream_t st = stream_of(ctx, q);
+        cudaEvent_t a;
+        if ((rc = timed_begin(ctx, st, &a))) return rc;
+        CK(launch_stencil2d_halo(kernel, a0.dtype, P_(1), P_(0), S, lbs, ubs, (int)fb.size(),
+                                 (int)job.interior.size(), job.batches[0], hp, ks, st));
+        count_launch(ctx);
+        ctx->cur_dev = q;
+        ctx->cur_phase = 1;
+        if ((rc = timed_end(ctx, st, kernel, a, 1))) return rc;
       } else if (kern && ctx->pulled_on_comm[q]) {
         // interior boxes while the pull is in flight, dependent boxes after it
         const PullJob& job = *ctx->cur_pull[q];
@@ -1074,6 +1124,7 @@ static hda_ctx_t* new_ctx(int P) {
   ctx->recv_cap.assign(P, 0);
   ctx->pulled_on_comm.assign(P, 0);
   ctx->cur_pull.assign(P, nullptr);
+  ctx->halo_job.assign(P, nullptr);
   return ctx;
 }
 

@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "kernels.cuh"
 #include "sync.cuh"
@@ -81,12 +82,8 @@ __device__ __forceinline__ void warp_copy(char* d, const char* s, int64_t n, int
   }
 }
 
-__global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ RunBatch b,
-                                                        const __grid_constant__ KSync ks) {
-  ks_pre(ks);
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+// warps [warp0, warp0+nwarps) of the caller process units warp0, warp0+nwarps, ...
+__device__ __forceinline__ void copy_units(const RunBatch& b, int64_t warp, int64_t nwarps, int lane) {
   for (int64_t u = warp; u < b.total_units; u += nwarps) {
     int k = 0;
     while (k + 1 < b.n && b.d[k + 1].unit_begin <= u) k++;
@@ -110,6 +107,15 @@ __global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ 
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) copy_runs_kernel(const __grid_constant__ RunBatch b,
+                                                        const __grid_constant__ KSync ks) {
+  ks_pre(ks);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  copy_units(b, warp, nwarps, lane);
   ks_post(ks);
 }
 
@@ -398,6 +404,89 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
   ks_post(ks);
 }
 
+// Fused halo-exchange stencil (one launch per step).  z-slice 0: NVLink pull blocks —
+// they wait for the writers' PROD words, copy every planned halo rectangle from the
+// peers' replicas into this replica, and the last of them releases a local word and the
+// writers' ACK words.  z-slices 1..: the stencil boxes (interior first, dependent strips
+// last); dependent blocks wait for the local word and read with L1-bypassing loads.
+// The pull blocks are dispatched first and wait on nothing inside the kernel, so the
+// dependent blocks' in-kernel wait always makes progress.
+struct PullPart {
+  unsigned long long* wait_ptr[8];
+  unsigned long long wait_val[8];
+  unsigned long long* ack_ptr[8];
+  int32_t nwait, nack, nblocks;
+  unsigned int* ctr;
+  unsigned long long* done_word;  // local
+  unsigned long long epoch;
+};
+
+template <typename T, int KIND, int ROWS>
+__global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
+    stencil2d_halo_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
+                          const __grid_constant__ Boxes2 bx, int32_t n_interior,
+                          const __grid_constant__ RunBatch pull, const __grid_constant__ PullPart pp,
+                          const __grid_constant__ KSync ks) {
+  const int z = blockIdx.z;
+  const int64_t bslice = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  if (z == 0) {
+    if (bslice < pp.nblocks) {
+      // RAW: the writers finished the call that produced these cells
+      if ((int)threadIdx.x < pp.nwait) {
+        const unsigned long long t0 = ks_timer();
+        while (ks_ld_acquire(pp.wait_ptr[threadIdx.x]) < pp.wait_val[threadIdx.x]) {
+          __nanosleep(32);
+          if ((long long)(ks_timer() - t0) > ks.timeout_ns) {
+            *reinterpret_cast<volatile int*>(ks.err) = -7;
+            __threadfence_system();
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      const int lane = threadIdx.x & 31;
+      copy_units(pull, (bslice * ST_THREADS + threadIdx.x) >> 5, ((int64_t)pp.nblocks * ST_THREADS) >> 5, lane);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(pp.ctr, 1u) == (unsigned)pp.nblocks - 1) {
+          *pp.ctr = 0;
+          __threadfence();
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.done_word), "l"(pp.epoch) : "memory");
+          for (int i = 0; i < pp.nack; i++)
+            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.ack_ptr[i]), "l"(pp.epoch) : "memory");
+        }
+      }
+    }
+    ks_post(ks);
+    return;
+  }
+  ks_pre(ks);  // WAR: peers finished reading the cells this launch overwrites
+  const int b = z - 1;
+  const bool inside = (int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b];
+  if (b >= n_interior) {
+    if (threadIdx.x == 0 && inside) {
+      const unsigned long long t0 = ks_timer();
+      while (ks_ld_acquire(pp.done_word) < pp.epoch) {
+        __nanosleep(32);
+        if ((long long)(ks_timer() - t0) > ks.timeout_ns) {
+          *reinterpret_cast<volatile int*>(ks.err) = -7;
+          __threadfence_system();
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    if (inside)
+      stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                          bx.rpb[b]);
+  } else if (inside) {
+    stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                         bx.rpb[b]);
+  }
+  ks_post(ks);
+}
+
 // scalar fallback for row pitches that are not 16-byte multiples (small test shapes)
 template <typename T, int KIND>
 __global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
@@ -489,6 +578,86 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     }
   }
   return cudaGetLastError();
+}
+
+template <typename T, int KIND>
+static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, const int64_t* const* lbs,
+                                 const int64_t* const* ubs, int nb, int n_interior, const RunBatch& pull,
+                                 const HaloPull& hp, const KSync& ks, cudaStream_t s) {
+  const int64_t ld = shape[2];
+  constexpr int V = V16<T>::n;
+  constexpr int ROWS = ST_ROWS;
+  Boxes2 bx;
+  bx.n = 0;
+  int gx = 1, gy = 1;
+  int ni = 0;
+  for (int i = 0; i < nb && bx.n < 8; i++) {
+    const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
+    if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
+    if (i < n_interior) ni++;
+    const int k = bx.n++;
+    bx.r0[k] = r0;
+    bx.r1[k] = r1;
+    bx.c0[k] = c0;
+    bx.c1[k] = c1;
+    bx.cbase[k] = c0 - (c0 % V);
+    const int64_t per_block = (int64_t)ST_THREADS * V;
+    bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
+  }
+  int64_t strips = 0, tiles16 = 0;
+  for (int k = 0; k < bx.n; k++) {
+    strips += bx.gx[k];
+    tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
+  }
+  const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
+  const bool one_wave = tiles16 < 8 * wave;
+  for (int k = 0; k < bx.n; k++) {
+    const int64_t rows = bx.r1[k] - bx.r0[k];
+    int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
+    if (one_wave && bx.c1[k] - bx.c0[k] > 64 && k < ni) {
+      gyk = std::max<int64_t>(1, wave / std::max<int64_t>(strips, 1));
+      gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
+    }
+    bx.rpb[k] = (rows + gyk - 1) / gyk;
+    bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
+    gx = std::max(gx, bx.gx[k]);
+    gy = std::max(gy, bx.gy[k]);
+  }
+  PullPart pp;
+  std::memset(&pp, 0, sizeof pp);
+  pp.nwait = hp.nwait;
+  pp.nack = hp.nack;
+  for (int i = 0; i < hp.nwait; i++) {
+    pp.wait_ptr[i] = hp.wait_ptr[i];
+    pp.wait_val[i] = hp.wait_val[i];
+  }
+  for (int i = 0; i < hp.nack; i++) pp.ack_ptr[i] = hp.ack_ptr[i];
+  pp.ctr = hp.ctr;
+  pp.done_word = hp.done_word;
+  pp.epoch = hp.epoch;
+  int64_t pb = (pull.total_units + 7) / 8;  // 8 warps per block
+  pb = std::max<int64_t>(1, std::min<int64_t>(pb, 64));
+  pp.nblocks = (int)std::min<int64_t>(pb, (int64_t)gx * gy);
+  if ((int64_t)gx * gy < pb) {  // make room in slice 0 for the pull blocks
+    gx = std::max<int>(gx, (int)pb);
+    pp.nblocks = (int)pb;
+  }
+  stencil2d_halo_kernel<T, KIND, ROWS><<<dim3(gx, gy, bx.n + 1), ST_THREADS, 0, s>>>(in, out, ld, bx, ni, pull, pp,
+                                                                                     ks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
+                                  const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,
+                                  const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s) {
+  if (kernel == 1) {
+    if (dtype == 0)
+      return launch_halo_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
+    return launch_halo_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
+  }
+  if (dtype == 0)
+    return launch_halo_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
+  return launch_halo_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
 }
 
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,

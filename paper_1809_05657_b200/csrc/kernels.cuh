@@ -78,6 +78,21 @@ cudaError_t launch_signal(const SignalList& l, cudaStream_t s);
 
 // user kernels over the work box [lb, ub) of one device's replica (padded 3-D shape)
 // 2-D stencils over nb (<= 8) boxes in ONE launch (lbs[i], ubs[i] front-padded 3-D)
+// Fused halo-exchange 2-D stencil (kernel 1 = JACOBI5, 3 = STENCIL9): pulls `pull`
+// (peer replica -> this replica) in its first blocks, then computes boxes
+// [0, n_interior) immediately and boxes [n_interior, nb) after the pull — one launch.
+struct HaloPull {
+  unsigned long long* wait_ptr[8];  // local PROD words of the sources
+  unsigned long long wait_val[8];
+  unsigned long long* ack_ptr[8];   // sources' ACK words for this reader
+  int32_t nwait, nack;
+  unsigned int* ctr;                // local counter
+  unsigned long long* done_word;    // local "pull done" word
+  unsigned long long epoch;
+};
+cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
+                                  const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,
+                                  const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s);
 // gate_word != NULL: boxes [first_gated, nb) wait for *gate_word >= gate_val (an
 // overlapped halo pull) inside the same launch
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
