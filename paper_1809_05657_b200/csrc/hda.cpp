@@ -915,7 +915,10 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     DevGuard g(true);
     const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
                                 kernel == KN_SCALE || kernel == KN_COPY;
-    const bool halo_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9;
+    // HDA_HALO_MODE: 0 (default) comm-stream pull + interior launch + boundary launch;
+    // 1 one fused launch (pull blocks + interior + gated strips); 2 gated two-stream.
+    static const int halo_mode = env_int("HDA_HALO_MODE", 0);
+    const bool halo_kernel = halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9);
     if ((rc = do_exchange(ctx, t, k, overlap_kernel, halo_kernel))) return rc;
     const TPart& pt = ctx->tr->part(part);
     for (int q = 0; q < ctx->P; q++) {
@@ -1020,7 +1023,8 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         bool joined = false;
         const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
         const bool stencil2d = kernel == KN_JACOBI5 || kernel == KN_STENCIL9;
-        if (stencil2d && job.interior.size() + job.dependent.size() <= 8) {
+        static const int halo_mode = env_int("HDA_HALO_MODE", 0);
+        if (halo_mode == 2 && stencil2d && job.interior.size() + job.dependent.size() <= 8) {
           // ONE launch: interior blocks first; the dependent strips' blocks (scheduled
           // last) wait in-kernel for the pull's local release word, then read the halo
           // with L1-bypassing loads.  The one-wave grid leaves every SM room for the

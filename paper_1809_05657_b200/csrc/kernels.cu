@@ -270,7 +270,8 @@ __device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
 // an overlapped halo exchange run as ONE launch
 struct Boxes2 {
   int64_t r0[8], r1[8], c0[8], c1[8], cbase[8];
-  int64_t rpb[8];  // rows per block (each block marches a contiguous row range)
+  int64_t rpb[8];     // rows per block (each block marches a contiguous row range)
+  int64_t tstart[9];  // flat-grid launches: first tile of each box
   int32_t gx[8], gy[8];
   int32_t n;
 };
@@ -278,13 +279,13 @@ struct Boxes2 {
 template <typename T, int KIND, int ROWS, bool CG>
 __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
                                                int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase,
-                                               int64_t rpb) {
+                                               int64_t rpb, int64_t xb, int64_t yb) {
   constexpr int V = V16<T>::n;
   constexpr int W = ST_GROUP + 2;
   const int lane = threadIdx.x & 31;
-  const int64_t col = cbase + ((int64_t)blockIdx.x * ST_THREADS + threadIdx.x) * V;
+  const int64_t col = cbase + (xb * ST_THREADS + threadIdx.x) * V;
   const bool live = col < ld;
-  const int64_t rs = r0 + (int64_t)blockIdx.y * rpb;
+  const int64_t rs = r0 + yb * rpb;
   const int64_t re = min(rs + rpb, r1);
   T w[W][V];
 
@@ -396,10 +397,10 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     __syncthreads();
     if (inside)
       stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                          bx.rpb[b]);
+                                          bx.rpb[b], blockIdx.x, blockIdx.y);
   } else if (inside) {
     stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                         bx.rpb[b]);
+                                         bx.rpb[b], blockIdx.x, blockIdx.y);
   }
   ks_post(ks);
 }
@@ -427,45 +428,46 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
                           const __grid_constant__ Boxes2 bx, int32_t n_interior,
                           const __grid_constant__ RunBatch pull, const __grid_constant__ PullPart pp,
                           const __grid_constant__ KSync ks) {
-  const int z = blockIdx.z;
-  const int64_t bslice = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  if (z == 0) {
-    if (bslice < pp.nblocks) {
-      // RAW: the writers finished the call that produced these cells
-      if ((int)threadIdx.x < pp.nwait) {
-        const unsigned long long t0 = ks_timer();
-        while (ks_ld_acquire(pp.wait_ptr[threadIdx.x]) < pp.wait_val[threadIdx.x]) {
-          __nanosleep(32);
-          if ((long long)(ks_timer() - t0) > ks.timeout_ns) {
-            *reinterpret_cast<volatile int*>(ks.err) = -7;
-            __threadfence_system();
-            break;
-          }
+  // flat grid: [0, nblocks) pull; then the tiles of box 0, 1, ... (interior boxes first)
+  const int64_t bid = blockIdx.x;
+  if (bid < pp.nblocks) {
+    // RAW: the writers finished the call that produced these cells
+    if ((int)threadIdx.x < pp.nwait) {
+      const unsigned long long t0 = ks_timer();
+      while (ks_ld_acquire(pp.wait_ptr[threadIdx.x]) < pp.wait_val[threadIdx.x]) {
+        __nanosleep(32);
+        if ((long long)(ks_timer() - t0) > ks.timeout_ns) {
+          *reinterpret_cast<volatile int*>(ks.err) = -7;
+          __threadfence_system();
+          break;
         }
       }
-      __syncthreads();
-      const int lane = threadIdx.x & 31;
-      copy_units(pull, (bslice * ST_THREADS + threadIdx.x) >> 5, ((int64_t)pp.nblocks * ST_THREADS) >> 5, lane);
-      __syncthreads();
-      if (threadIdx.x == 0) {
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    copy_units(pull, (bid * ST_THREADS + threadIdx.x) >> 5, ((int64_t)pp.nblocks * ST_THREADS) >> 5, lane);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(pp.ctr, 1u) == (unsigned)pp.nblocks - 1) {
+        *pp.ctr = 0;
         __threadfence();
-        if (atomicAdd(pp.ctr, 1u) == (unsigned)pp.nblocks - 1) {
-          *pp.ctr = 0;
-          __threadfence();
-          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.done_word), "l"(pp.epoch) : "memory");
-          for (int i = 0; i < pp.nack; i++)
-            asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.ack_ptr[i]), "l"(pp.epoch) : "memory");
-        }
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.done_word), "l"(pp.epoch) : "memory");
+        for (int i = 0; i < pp.nack; i++)
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.ack_ptr[i]), "l"(pp.epoch) : "memory");
       }
     }
     ks_post(ks);
     return;
   }
   ks_pre(ks);  // WAR: peers finished reading the cells this launch overwrites
-  const int b = z - 1;
-  const bool inside = (int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b];
+  const int64_t t = bid - pp.nblocks;
+  int b = 0;
+  while (b + 1 < bx.n && bx.tstart[b + 1] <= t) b++;
+  const int64_t local = t - bx.tstart[b];
+  const int64_t xb = local % bx.gx[b], yb = local / bx.gx[b];
   if (b >= n_interior) {
-    if (threadIdx.x == 0 && inside) {
+    if (threadIdx.x == 0) {
       const unsigned long long t0 = ks_timer();
       while (ks_ld_acquire(pp.done_word) < pp.epoch) {
         __nanosleep(32);
@@ -477,12 +479,11 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
       }
     }
     __syncthreads();
-    if (inside)
-      stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                          bx.rpb[b]);
-  } else if (inside) {
+    stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b], bx.rpb[b],
+                                        xb, yb);
+  } else {
     stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                         bx.rpb[b]);
+                                         bx.rpb[b], xb, yb);
   }
   ks_post(ks);
 }
@@ -589,7 +590,6 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
   constexpr int ROWS = ST_ROWS;
   Boxes2 bx;
   bx.n = 0;
-  int gx = 1, gy = 1;
   int ni = 0;
   for (int i = 0; i < nb && bx.n < 8; i++) {
     const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
@@ -604,24 +604,14 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     const int64_t per_block = (int64_t)ST_THREADS * V;
     bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
   }
-  int64_t strips = 0, tiles16 = 0;
-  for (int k = 0; k < bx.n; k++) {
-    strips += bx.gx[k];
-    tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
-  }
-  const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
-  const bool one_wave = tiles16 < 8 * wave;
+  // 16-row tiles on a flat grid: small blocks balance dynamically around the few
+  // co-resident pull blocks (a one-wave layout got pushed into a second wave)
+  bx.tstart[0] = 0;
   for (int k = 0; k < bx.n; k++) {
     const int64_t rows = bx.r1[k] - bx.r0[k];
-    int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
-    if (one_wave && bx.c1[k] - bx.c0[k] > 64 && k < ni) {
-      gyk = std::max<int64_t>(1, wave / std::max<int64_t>(strips, 1));
-      gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
-    }
-    bx.rpb[k] = (rows + gyk - 1) / gyk;
-    bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
-    gx = std::max(gx, bx.gx[k]);
-    gy = std::max(gy, bx.gy[k]);
+    bx.rpb[k] = ST_ROWS;
+    bx.gy[k] = (int)((rows + ST_ROWS - 1) / ST_ROWS);
+    bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
   }
   PullPart pp;
   std::memset(&pp, 0, sizeof pp);
@@ -636,14 +626,9 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
   pp.done_word = hp.done_word;
   pp.epoch = hp.epoch;
   int64_t pb = (pull.total_units + 7) / 8;  // 8 warps per block
-  pb = std::max<int64_t>(1, std::min<int64_t>(pb, 64));
-  pp.nblocks = (int)std::min<int64_t>(pb, (int64_t)gx * gy);
-  if ((int64_t)gx * gy < pb) {  // make room in slice 0 for the pull blocks
-    gx = std::max<int>(gx, (int)pb);
-    pp.nblocks = (int)pb;
-  }
-  stencil2d_halo_kernel<T, KIND, ROWS><<<dim3(gx, gy, bx.n + 1), ST_THREADS, 0, s>>>(in, out, ld, bx, ni, pull, pp,
-                                                                                     ks);
+  pp.nblocks = (int)std::max<int64_t>(1, std::min<int64_t>(pb, 64));
+  const int64_t grid = pp.nblocks + bx.tstart[bx.n];
+  stencil2d_halo_kernel<T, KIND, ROWS><<<(unsigned)grid, ST_THREADS, 0, s>>>(in, out, ld, bx, ni, pull, pp, ks);
   return cudaGetLastError();
 }
 

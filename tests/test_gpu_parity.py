@@ -333,6 +333,9 @@ def test_multi_gpu_single_process(H, P):
             for s in range(6):
                 src, dst = (X, Y) if s % 2 == 0 else (Y, X)
                 be.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+            for s in range(4):
+                src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+                be.apply(H.K_STENCIL9, part, [(dst, [], [(0, 0)]), (src, N9, [])])
             be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
         assert_replicas(h, w, [X, Y], P)
         h.close()
@@ -353,6 +356,22 @@ def test_multi_gpu_single_process(H, P):
                 be.apply(H.K_SCALE, rp, [(Z, [(0, 0)], [(0, 0)])], [0.5])
         assert_replicas(h, w, [Z], P)
         h.close()
+
+
+@pytest.mark.skipif("ngpus() < 2")
+@pytest.mark.parametrize("mode", [1, 2])
+def test_multi_gpu_halo_modes(mode):
+    """The optional 2-D halo launch shapes (HDA_HALO_MODE 1: pull blocks + interior +
+    gated strips in one launch; 2: gated boundary blocks in the interior launch) give
+    the same replicas as the default; the mode is read once per process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, HDA_HALO_MODE=str(mode))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        f"{__file__}::test_multi_gpu_single_process"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
 # ------------------------------------------------------------------ 2MM (SURVEY §8(f)-1)
@@ -453,4 +472,23 @@ def test_absolute_sections_triangular_gpu(H):
     assert_same_msgs(h, w)
     assert len(w.msgs()) > 0
     assert_replicas(h, w, [X], P)
+    h.close()
+
+
+def test_trace_rows(H):
+    """hda_set_trace / hda_trace: one exchange + one kernel span per call, ordered."""
+    n, P = 64, 2
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    X = h.create(H.F64, (n, n), synth.uniform(1, (n, n)))
+    Y = h.create(H.F64, (n, n))
+    part = h.partition(H.ROW, (n, n), (1, 1), (n - 1, n - 1))
+    h.set_trace(True)
+    for s in range(4):
+        src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+        h.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+    t = h.trace()
+    h.set_trace(False)
+    assert len(t) >= 8  # >= one kernel span per device per call
+    assert (t[:, 4] >= t[:, 3]).all() and (t[:, 3] >= 0).all()
+    assert set(t[:, 1].astype(int)) == {0, 1}
     h.close()
