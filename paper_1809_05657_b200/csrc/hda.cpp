@@ -599,7 +599,6 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
           ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
           ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
         }
-      if (comm) ks_sig(post, ctx->dev[q].sync + SW_PULLDONE);  // gates the dependent strips
       int rc;
       cudaEvent_t a = nullptr;
       const size_t nb = job.batches.size();
@@ -916,7 +915,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
                                 kernel == KN_SCALE || kernel == KN_COPY;
     // HDA_HALO_MODE: 0 (default) comm-stream pull + interior launch + boundary launch;
-    // 1 one fused launch (pull blocks + interior + gated strips); 2 gated two-stream.
+    // 1 one fused launch (pull blocks + interior + gated strips).
     static const int halo_mode = env_int("HDA_HALO_MODE", 0);
     const bool halo_kernel = halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9);
     if ((rc = do_exchange(ctx, t, k, overlap_kernel, halo_kernel))) return rc;
@@ -1022,42 +1021,6 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         Gpu& g = ctx->gpus[ctx->dev[q].gpu];
         bool joined = false;
         const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
-        const bool stencil2d = kernel == KN_JACOBI5 || kernel == KN_STENCIL9;
-        static const int halo_mode = env_int("HDA_HALO_MODE", 0);
-        if (halo_mode == 2 && stencil2d && job.interior.size() + job.dependent.size() <= 8) {
-          // ONE launch: interior blocks first; the dependent strips' blocks (scheduled
-          // last) wait in-kernel for the pull's local release word, then read the halo
-          // with L1-bypassing loads.  The one-wave grid leaves every SM room for the
-          // pull's CTAs, so the wait cannot starve the pull.
-          const CallInfo& ci = *t->info;
-          const TArray& a0 = ctx->tr->array(ci.param_array[0]);
-          int64_t S[3];
-          front_shape(a0.ndim, a0.shape, S);
-          std::vector<Box> fb;
-          for (const Box& b : job.interior) fb.push_back(front_box(a0.ndim, b));
-          for (const Box& b : job.dependent) fb.push_back(front_box(a0.ndim, b));
-          const int64_t* lbs[8];
-          const int64_t* ubs[8];
-          for (size_t i = 0; i < fb.size(); i++) {
-            lbs[i] = fb[i].lb;
-            ubs[i] = fb[i].ub;
-          }
-          auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
-          cudaEvent_t a;
-          if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-          const unsigned long long* gw = ctx->dev[q].sync + SW_PULLDONE;
-          const int nfb = (int)fb.size(), ni = (int)job.interior.size();
-          if (kernel == KN_JACOBI5)
-            CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, lbs, ubs, nfb, ks, g.stream, gw, k, ni));
-          else
-            CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, lbs, ubs, nfb, ks, g.stream, gw, k, ni));
-          count_launch(ctx);
-          ctx->cur_dev = q;
-          ctx->cur_phase = 1;
-          if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
-          CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));  // keep later stream work ordered
-          joined = true;
-        } else {
         if (has_i) {
           cudaEvent_t a;
           if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
@@ -1075,7 +1038,6 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
           ctx->cur_dev = q;
           ctx->cur_phase = 3;
           if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
-        }
         }
         if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
         ctx->pulled_on_comm[q] = 0;

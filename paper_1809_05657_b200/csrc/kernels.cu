@@ -366,41 +366,26 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
   }
 }
 
-// gate: boxes with index >= first_gated read cells an overlapped halo pull is writing
-// concurrently; their blocks (scheduled last) wait until *gate >= gate_val (released by
-// the pull kernel's last CTA) and read with L1-bypassing loads.
-struct Gate {
-  const unsigned long long* word;
-  unsigned long long val;
-  int32_t first_gated;
-};
+// flat 1-D grid over the tiles of up to 8 boxes (no empty blocks for mixed box shapes)
+__device__ __forceinline__ void tile_of(const Boxes2& bx, int64_t t, int& b, int64_t& xb, int64_t& yb) {
+  b = 0;
+  while (b + 1 < bx.n && bx.tstart[b + 1] <= t) b++;
+  const int64_t local = t - bx.tstart[b];
+  xb = local % bx.gx[b];
+  yb = local / bx.gx[b];
+}
 
 template <typename T, int KIND, int ROWS>
 __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     stencil2d_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld, const __grid_constant__ Boxes2 bx,
-                     const __grid_constant__ KSync ks, const Gate gate) {
+                     const __grid_constant__ KSync ks) {
   ks_pre(ks);
-  const int b = blockIdx.z;
-  const bool inside = (int)blockIdx.x < bx.gx[b] && (int)blockIdx.y < bx.gy[b];  // block-uniform
-  if (b >= gate.first_gated) {
-    if (threadIdx.x == 0 && inside) {
-      const unsigned long long t0 = ks_timer();
-      while (ks_ld_acquire(gate.word) < gate.val) {
-        __nanosleep(64);
-        if ((long long)(ks_timer() - t0) > ks.timeout_ns) {
-          *reinterpret_cast<volatile int*>(ks.err) = -7;
-          __threadfence_system();
-          break;
-        }
-      }
-    }
-    __syncthreads();
-    if (inside)
-      stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                          bx.rpb[b], blockIdx.x, blockIdx.y);
-  } else if (inside) {
+  if (bx.n > 0) {
+    int b;
+    int64_t xb, yb;
+    tile_of(bx, blockIdx.x, b, xb, yb);
     stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                         bx.rpb[b], blockIdx.x, blockIdx.y);
+                                         bx.rpb[b], xb, yb);
   }
   ks_post(ks);
 }
@@ -423,7 +408,7 @@ struct PullPart {
 };
 
 template <typename T, int KIND, int ROWS>
-__global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
+__global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs the registers of minB 4
     stencil2d_halo_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
                           const __grid_constant__ Boxes2 bx, int32_t n_interior,
                           const __grid_constant__ RunBatch pull, const __grid_constant__ PullPart pp,
@@ -461,11 +446,9 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     return;
   }
   ks_pre(ks);  // WAR: peers finished reading the cells this launch overwrites
-  const int64_t t = bid - pp.nblocks;
-  int b = 0;
-  while (b + 1 < bx.n && bx.tstart[b + 1] <= t) b++;
-  const int64_t local = t - bx.tstart[b];
-  const int64_t xb = local % bx.gx[b], yb = local / bx.gx[b];
+  int b;
+  int64_t xb, yb;
+  tile_of(bx, bid - pp.nblocks, b, xb, yb);
   if (b >= n_interior) {
     if (threadIdx.x == 0) {
       const unsigned long long t0 = ks_timer();
@@ -509,9 +492,7 @@ __global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict_
 
 template <typename T, int KIND>
 static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* const* lbs,
-                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
-                                      const unsigned long long* gate_word, unsigned long long gate_val,
-                                      int first_gated) {
+                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
   const int64_t ld = shape[2];
   constexpr int V = V16<T>::n;
   const bool vec = (ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
@@ -520,12 +501,9 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     constexpr int ROWS = ST_ROWS;
     Boxes2 bx;
     bx.n = 0;
-    int gx = 1, gy = 1;
-    int gated_from = 8;
-    for (int i = 0; i < nb; i++) {
+    for (int i = 0; i < nb && bx.n < 8; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
       if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
-      if (i >= first_gated && gated_from == 8) gated_from = bx.n;
       const int k = bx.n++;
       bx.r0[k] = r0;
       bx.r1[k] = r1;
@@ -548,6 +526,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     }
     const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
     const bool one_wave = tiles16 < 8 * wave;
+    bx.tstart[0] = 0;
     for (int k = 0; k < bx.n; k++) {
       const int64_t rows = bx.r1[k] - bx.r0[k];
       int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
@@ -557,15 +536,11 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       }
       bx.rpb[k] = (rows + gyk - 1) / gyk;
       bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
-      gx = std::max(gx, bx.gx[k]);
-      gy = std::max(gy, bx.gy[k]);
+      bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
     }
-    if (bx.n == 0) {  // nothing to compute, but the sync words must still move
-      bx.n = 1;
-      bx.gx[0] = bx.gy[0] = 0;
-    }
-    Gate gate{gate_word, gate_val, gate_word ? gated_from : 8};
-    stencil2d_kernel<T, KIND, ROWS><<<dim3(gx, gy, bx.n), ST_THREADS, 0, s>>>(in, out, ld, bx, ks, gate);
+    // bx.n == 0: nothing to compute, but the sync words must still move (one block)
+    const int64_t grid = bx.n ? bx.tstart[bx.n] : 1;
+    stencil2d_kernel<T, KIND, ROWS><<<(unsigned)grid, ST_THREADS, 0, s>>>(in, out, ld, bx, ks);
   } else {
     for (int i = 0; i < nb; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
@@ -646,23 +621,15 @@ cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* o
 }
 
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
-                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
-                           const unsigned long long* gate_word, unsigned long long gate_val, int first_gated) {
-  if (dtype == 0)
-    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s, gate_word,
-                                         gate_val, first_gated);
-  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s, gate_word, gate_val,
-                                      first_gated);
+                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+  if (dtype == 0) return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
+  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
 }
 
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
-                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
-                            const unsigned long long* gate_word, unsigned long long gate_val, int first_gated) {
-  if (dtype == 0)
-    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s, gate_word,
-                                         gate_val, first_gated);
-  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s, gate_word, gate_val,
-                                      first_gated);
+                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+  if (dtype == 0) return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
+  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
 }
 
 // =====================================================================================

@@ -93,16 +93,13 @@ struct HaloPull {
 cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
                                   const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,
                                   const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s);
-// gate_word != NULL: boxes [first_gated, nb) wait for *gate_word >= gate_val (an
-// overlapped halo pull) inside the same launch
+// up to 8 boxes in one launch (flat grid of tiles)
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
                            const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
-                           cudaStream_t s, const unsigned long long* gate_word = nullptr,
-                           unsigned long long gate_val = 0, int first_gated = 8);
+                           cudaStream_t s);
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
-                            cudaStream_t s, const unsigned long long* gate_word = nullptr,
-                            unsigned long long gate_val = 0, int first_gated = 8);
+                            cudaStream_t s);
 cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb,

@@ -359,11 +359,11 @@ def test_multi_gpu_single_process(H, P):
 
 
 @pytest.mark.skipif("ngpus() < 2")
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1])
 def test_multi_gpu_halo_modes(mode):
-    """The optional 2-D halo launch shapes (HDA_HALO_MODE 1: pull blocks + interior +
-    gated strips in one launch; 2: gated boundary blocks in the interior launch) give
-    the same replicas as the default; the mode is read once per process."""
+    """The optional fused 2-D halo launch (HDA_HALO_MODE=1: pull blocks + interior +
+    gated boundary strips in one launch) gives the same replicas as the default
+    three-launch shape; the mode is read once per process."""
     import os
     import subprocess
     import sys
