@@ -91,6 +91,9 @@ struct PullJob {
   std::vector<Box> interior, dependent;
   std::vector<cudaMemcpy3DParms> ce;  // AUTO transport: bulk messages on the copy engine
 };
+struct PendEntry {
+  int array, src, dst;
+};
 struct PackJob {
   int src;
   std::vector<int> dsts;
@@ -113,6 +116,9 @@ struct ExecPlan {
   int transport = HDA_XPORT_FUSED;
   std::vector<PullJob> pulls;
   std::vector<PackJob> packs;
+  // every (array, src, dst) read of this call, local reader or not: in SPMD the writer's
+  // rank must know its REMOTE readers too, to wait for their ACKs before overwriting
+  std::vector<PendEntry> reads;
   std::vector<RecvJob> recvs;
 };
 
@@ -313,7 +319,14 @@ static KSync ks_empty(hda_ctx_t* ctx) {
   k.ctr = nullptr;
   k.err = ctx->err_host;
   k.timeout_ns = ctx->timeout_ns;
+  k.delay_ns = 0;
   return k;
+}
+// test hook: every pull (the reader side of an exchange) sleeps this long after its
+// RAW waits, so a missing WAR wait on the writer shows up as a parity failure
+static long long pull_delay_ns() {
+  static const long long v = 1000LL * env_int("HDA_DEBUG_PULL_DELAY_US", 0);
+  return v;
 }
 static void ks_wait(KSync& k, unsigned long long* p, unsigned long long v) {
   if (v == 0) return;
@@ -366,6 +379,12 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
   ep.staged = ctx->transport == HDA_XPORT_STAGED;
   ep.transport = ctx->transport;
   if (t->msgs.empty()) return HDA_OK;
+  for (const Msg& m : t->msgs) {
+    bool seen = false;
+    for (const PendEntry& e : ep.reads)
+      if (e.array == m.array && e.src == m.src && e.dst == m.dst) seen = true;
+    if (!seen) ep.reads.push_back({m.array, m.src, m.dst});
+  }
   if (!ep.staged) {
     for (int q = 0; q < P; q++) {
       if (!ctx->dev[q].local) continue;
@@ -571,6 +590,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
     ep = &scratch;
   }
   if (!ep->staged) {
+    for (const PendEntry& e : ep->reads) ctx->pend[e.array][e.src][e.dst] = k;
     for (PullJob& job : ep->pulls) {
       const int q = job.dst;
       CK(cudaSetDevice(ordinal_of(ctx, q)));
@@ -608,9 +628,10 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
         std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
         std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
         w.nwait = pre.nwait;
+        w.delay_ns = pull_delay_ns();
         RunBatch empty;
         std::memset(&empty, 0, sizeof empty);
-        if (w.nwait) {
+        if (w.nwait || w.delay_ns) {
           CK(launch_copy_runs(empty, w, st));
           count_launch(ctx);
         }
@@ -628,6 +649,7 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
           std::memcpy(ks.wait_ptr, pre.wait_ptr, sizeof ks.wait_ptr);
           std::memcpy(ks.wait_val, pre.wait_val, sizeof ks.wait_val);
           ks.nwait = pre.nwait;
+          ks.delay_ns = pull_delay_ns();
         }
         if (i + 1 == nb) {
           std::memcpy(ks.sig_ptr, post.sig_ptr, sizeof ks.sig_ptr);
@@ -1005,6 +1027,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         hp.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
         hp.done_word = ctx->dev[q].sync + SW_PULLDONE;
         hp.epoch = k;
+        hp.delay_ns = pull_delay_ns();
         auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
         cudaStream_t st = stream_of(ctx, q);
         cudaEvent_t a;

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "sync.cuh"
@@ -244,6 +245,15 @@ static int sm_count_dev() {
   return n[dev];
 }
 
+// HDA_ONE_WAVE=0 disables the one-wave row-range layout (A/B measurements)
+static bool one_wave_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("HDA_ONE_WAVE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
 constexpr int ST_ROWS = 16;      // rows per block
@@ -405,6 +415,7 @@ struct PullPart {
   unsigned int* ctr;
   unsigned long long* done_word;  // local
   unsigned long long epoch;
+  long long delay_ns;
 };
 
 template <typename T, int KIND, int ROWS>
@@ -427,6 +438,10 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs t
           break;
         }
       }
+    }
+    if (pp.delay_ns && threadIdx.x == 0) {  // test hook
+      const unsigned long long t0 = ks_timer();
+      while ((long long)(ks_timer() - t0) < pp.delay_ns) __nanosleep(1000);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -525,7 +540,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
     }
     const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
-    const bool one_wave = tiles16 < 8 * wave;
+    const bool one_wave = one_wave_enabled() && tiles16 < 8 * wave;
     bx.tstart[0] = 0;
     for (int k = 0; k < bx.n; k++) {
       const int64_t rows = bx.r1[k] - bx.r0[k];
@@ -579,13 +594,34 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     const int64_t per_block = (int64_t)ST_THREADS * V;
     bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
   }
-  // 16-row tiles on a flat grid: small blocks balance dynamically around the few
-  // co-resident pull blocks (a one-wave layout got pushed into a second wave)
+  int64_t pb = (pull.total_units + 7) / 8;  // 8 warps per block
+  const int npull = (int)std::max<int64_t>(1, std::min<int64_t>(pb, 64));
+  // Interior boxes: when the GPU's share is under ~8 waves of 16-row tiles, ONE wave
+  // of row-range blocks sized to the slots the pull blocks leave free (blocks that
+  // miss the first wave would double the step); the boundary strips keep 16-row tiles
+  // and run in the slots the pull blocks vacate.
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_halo_kernel<T, KIND, ROWS>, ST_THREADS, 0);
+    if (occ <= 0) occ = 1;
+  }
+  const int64_t wave = (int64_t)sm_count_dev() * occ;
+  int64_t tiles16 = 0, strips_i = 0;
+  for (int k = 0; k < bx.n; k++) {
+    tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
+    if (k < ni && bx.c1[k] - bx.c0[k] > 64) strips_i += bx.gx[k];
+  }
+  const bool one_wave = one_wave_enabled() && tiles16 < 8 * wave && strips_i > 0 && wave - npull >= strips_i;
   bx.tstart[0] = 0;
   for (int k = 0; k < bx.n; k++) {
     const int64_t rows = bx.r1[k] - bx.r0[k];
-    bx.rpb[k] = ST_ROWS;
-    bx.gy[k] = (int)((rows + ST_ROWS - 1) / ST_ROWS);
+    int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
+    if (one_wave && k < ni && bx.c1[k] - bx.c0[k] > 64) {
+      gyk = std::max<int64_t>(1, (wave - npull) / strips_i);
+      gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
+    }
+    bx.rpb[k] = (rows + gyk - 1) / gyk;
+    bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
     bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
   }
   PullPart pp;
@@ -600,8 +636,8 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
   pp.ctr = hp.ctr;
   pp.done_word = hp.done_word;
   pp.epoch = hp.epoch;
-  int64_t pb = (pull.total_units + 7) / 8;  // 8 warps per block
-  pp.nblocks = (int)std::max<int64_t>(1, std::min<int64_t>(pb, 64));
+  pp.delay_ns = hp.delay_ns;
+  pp.nblocks = npull;
   const int64_t grid = pp.nblocks + bx.tstart[bx.n];
   stencil2d_halo_kernel<T, KIND, ROWS><<<(unsigned)grid, ST_THREADS, 0, s>>>(in, out, ld, bx, ni, pull, pp, ks);
   return cudaGetLastError();

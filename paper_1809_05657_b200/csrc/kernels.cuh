@@ -64,6 +64,7 @@ struct KSync {
   long long timeout_ns;
   int32_t nwait, nsig;
   int32_t relaxed;  // experiment: signal with st.relaxed.sys after a gpu-scope fence
+  long long delay_ns;  // test hook (HDA_DEBUG_PULL_DELAY_US): pulls sleep after their waits
 };
 
 struct BoxList {  // boxes in element coordinates of a 3-D padded shape
@@ -89,6 +90,7 @@ struct HaloPull {
   unsigned int* ctr;                // local counter
   unsigned long long* done_word;    // local "pull done" word
   unsigned long long epoch;
+  long long delay_ns;               // test hook (see KSync::delay_ns)
 };
 cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
                                   const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,

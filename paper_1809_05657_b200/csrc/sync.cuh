@@ -24,8 +24,12 @@ __device__ __forceinline__ unsigned long long ks_timer() {
 }
 
 __device__ __forceinline__ void ks_pre(const KSync& s) {
-  if (s.nwait == 0) return;
+  if (s.nwait == 0 && s.delay_ns == 0) return;
   const int tid = threadIdx.x + threadIdx.y * blockDim.x + threadIdx.z * blockDim.x * blockDim.y;
+  if (s.delay_ns && tid == 0) {  // test hook: a slow reader widens every WAR window
+    const unsigned long long t0 = ks_timer();
+    while ((long long)(ks_timer() - t0) < s.delay_ns) __nanosleep(1000);
+  }
   if (tid < s.nwait) {
     const unsigned long long t0 = ks_timer();
     while (ks_ld_acquire(s.wait_ptr[tid]) < s.wait_val[tid]) {

@@ -23,8 +23,10 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, env1):
     try:
+        if rank == 1:  # rank 1 only: an asymmetric slow reader opens the WAR window
+            os.environ.update(env1)
         import torch
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -98,7 +100,12 @@ def _worker(rank, world, port, q):
         q.put((rank, ["exception", traceback.format_exc()], 0, 0))
 
 
-def test_spmd_two_gpus():
+# HDA_DEBUG_PULL_DELAY_US makes rank 1's pulls sleep after their RAW waits: a writer
+# that overwrote cells without waiting for rank 1's ACK would break parity.
+@pytest.mark.parametrize("env1", [{}, {"HDA_DEBUG_PULL_DELAY_US": "300"},
+                                  {"HDA_DEBUG_PULL_DELAY_US": "300", "HDA_HALO_MODE": "1"}],
+                         ids=["plain", "slow-reader", "slow-reader-fused"])
+def test_spmd_two_gpus(env1):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
@@ -106,7 +113,7 @@ def test_spmd_two_gpus():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, env1)) for r in range(world)]
     for p in ps:
         p.start()
     out = [q.get(timeout=240) for _ in ps]
