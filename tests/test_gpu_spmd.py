@@ -66,6 +66,14 @@ def _worker(rank, world, port, q, env1):
             be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
             be.apply(H.K_SCALE, full, [(X, [(0, 0)], [(0, 0)])], [0.5])
         check("repart", [X])
+        # WAR: rank 1 pulls X's top-right block from rank 0 (COPY on COL), then rank 0
+        # rescales its own rows of X in place — needing nothing from rank 1, only its ACK
+        for it in range(3):
+            for be in (h, w):
+                be.write(X, full, u0 + it)
+                be.apply(H.K_COPY, colp, [(Y, [], [(0, 0)]), (X, [(0, 0)], [])])
+                be.apply(H.K_SCALE, full, [(X, [(0, 0)], [(0, 0)])], [2.0])
+            check(f"war{it}", [X, Y])
         # bulk ROW<->COL blocks (>= 1 MiB) through the copy engine under AUTO
         big = (1024, 2048)
         v = synth.uniform(8, big, "f32")
