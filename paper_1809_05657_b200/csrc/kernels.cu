@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstring>
 #include <cstdlib>
+#include <utility>
 
 #include "kernels.cuh"
 #include "sync.cuh"
@@ -254,6 +255,30 @@ static bool one_wave_enabled() {
   return v != 0;
 }
 
+// launch with the programmatic-stream-serialization attribute; only for kernels whose
+// first statement is pdl_enter() (sync.cuh).  HDA_PDL=0 disables it.
+static bool pdl_enabled() {
+  static const int v = [] {
+    const char* e = std::getenv("HDA_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
 constexpr int ST_ROWS = 16;      // rows per block
@@ -389,6 +414,7 @@ template <typename T, int KIND, int ROWS>
 __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     stencil2d_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld, const __grid_constant__ Boxes2 bx,
                      const __grid_constant__ KSync ks) {
+  pdl_enter();
   ks_pre(ks);
   if (bx.n > 0) {
     int b;
@@ -424,6 +450,7 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs t
                           const __grid_constant__ Boxes2 bx, int32_t n_interior,
                           const __grid_constant__ RunBatch pull, const __grid_constant__ PullPart pp,
                           const __grid_constant__ KSync ks) {
+  pdl_enter();
   // flat grid: [0, nblocks) pull; then the tiles of box 0, 1, ... (interior boxes first)
   const int64_t bid = blockIdx.x;
   if (bid < pp.nblocks) {
@@ -555,7 +582,9 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     }
     // bx.n == 0: nothing to compute, but the sync words must still move (one block)
     const int64_t grid = bx.n ? bx.tstart[bx.n] : 1;
-    stencil2d_kernel<T, KIND, ROWS><<<(unsigned)grid, ST_THREADS, 0, s>>>(in, out, ld, bx, ks);
+    cudaError_t e = launch_pdl(stencil2d_kernel<T, KIND, ROWS>, dim3((unsigned)grid), dim3(ST_THREADS), s, in, out,
+                               ld, bx, ks);
+    if (e != cudaSuccess) return e;
   } else {
     for (int i = 0; i < nb; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
@@ -639,8 +668,8 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
   pp.delay_ns = hp.delay_ns;
   pp.nblocks = npull;
   const int64_t grid = pp.nblocks + bx.tstart[bx.n];
-  stencil2d_halo_kernel<T, KIND, ROWS><<<(unsigned)grid, ST_THREADS, 0, s>>>(in, out, ld, bx, ni, pull, pp, ks);
-  return cudaGetLastError();
+  return launch_pdl(stencil2d_halo_kernel<T, KIND, ROWS>, dim3((unsigned)grid), dim3(ST_THREADS), s, in, out, ld,
+                    bx, ni, pull, pp, ks);
 }
 
 cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
@@ -684,6 +713,7 @@ __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ 
                                                          int64_t n2, int64_t z0, int64_t z1, int64_t y0, int64_t y1,
                                                          int64_t x0, int64_t x1, int64_t xbase,
                                                          const __grid_constant__ KSync ks) {
+  pdl_enter();
   ks_pre(ks);
   constexpr int V = V16<T>::n;
   const int lane = threadIdx.x & 31;
@@ -791,7 +821,9 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
     const int64_t per = 256 * V;
     dim3 grid((unsigned)((ub[2] - xbase + per - 1) / per), (unsigned)((ub[1] - lb[1] + S3_R - 1) / S3_R),
               (unsigned)((ub[0] - lb[0] + S3_ZCH - 1) / S3_ZCH));
-    stencil7_kernel<T><<<grid, 256, 0, s>>>(in, out, n1, n2, lb[0], ub[0], lb[1], ub[1], lb[2], ub[2], xbase, ks);
+    cudaError_t e = launch_pdl(stencil7_kernel<T>, grid, dim3(256), s, in, out, n1, n2, lb[0], ub[0], lb[1], ub[1],
+                               lb[2], ub[2], xbase, ks);
+    if (e != cudaSuccess) return e;
   } else {
     dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));
     stencil7_scalar_kernel<T><<<grid, 128, 0, s>>>(in, out, n1, n2, lb[0], lb[1], ub[1], lb[2], ub[2], ks);

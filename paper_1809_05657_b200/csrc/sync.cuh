@@ -23,6 +23,16 @@ __device__ __forceinline__ unsigned long long ks_timer() {
   return t;
 }
 
+// Programmatic dependent launch: kernels launched with launch_pdl() begin here.  The
+// wait returns once the previous kernel on the stream has completed and its writes are
+// visible (a no-op without the launch attribute); the trigger then lets the NEXT
+// kernel's CTAs be dispatched into the slots this grid's tail frees, so the launch
+// gap and CTA ramp of back-to-back stencil steps overlap the tail.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void ks_pre(const KSync& s) {
   if (s.nwait == 0 && s.delay_ns == 0) return;
   const int tid = threadIdx.x + threadIdx.y * blockDim.x + threadIdx.z * blockDim.x * blockDim.y;
