@@ -726,6 +726,9 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
 // WAR before device q overwrites cells of the arrays it defines: every peer that
 // pulled those arrays from q must have acknowledged the pull
 static void war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q, KSync& ks) {
+  // HDA_DEBUG_NO_WAR=1 drops the WAR waits: UNSAFE, measurement of their cost only
+  static const int no_war = env_int("HDA_DEBUG_NO_WAR", 0);
+  if (no_war) return;
   for (size_t i = 0; i < ci.arrays.size(); i++) {
     if (ci.ldef[i][q].empty()) continue;
     auto& row = ctx->pend[ci.arrays[i]][q];
