@@ -939,10 +939,13 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     DevGuard g(true);
     const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
                                 kernel == KN_SCALE || kernel == KN_COPY;
-    // HDA_HALO_MODE: 0 (default) comm-stream pull + interior launch + boundary launch;
-    // 1 one fused launch (pull blocks + interior + gated strips).
-    static const int halo_mode = env_int("HDA_HALO_MODE", 0);
-    const bool halo_kernel = halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9);
+    // HDA_HALO_MODE: 1 one fused launch (pull blocks + interior + gated boundary strips);
+    // 0 comm-stream pull + interior launch + boundary launch; -1 (default) fused for the
+    // 5-point Jacobi, three launches for the 9-point stencil (measured on 4 B200s,
+    // profiles/r01/README.md: Jacobi 1220 vs 1179 GPoints/s, 9-point 953 vs 1171).
+    static const int halo_mode = env_int("HDA_HALO_MODE", -1);
+    const bool halo_kernel = (halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9)) ||
+                             (halo_mode == -1 && kernel == KN_JACOBI5);
     if ((rc = do_exchange(ctx, t, k, overlap_kernel, halo_kernel))) return rc;
     const TPart& pt = ctx->tr->part(part);
     for (int q = 0; q < ctx->P; q++) {

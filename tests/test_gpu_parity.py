@@ -359,11 +359,12 @@ def test_multi_gpu_single_process(H, P):
 
 
 @pytest.mark.skipif("ngpus() < 2")
-@pytest.mark.parametrize("mode", [1])
+@pytest.mark.parametrize("mode", [0, 1])
 def test_multi_gpu_halo_modes(mode):
-    """The optional fused 2-D halo launch (HDA_HALO_MODE=1: pull blocks + interior +
-    gated boundary strips in one launch) gives the same replicas as the default
-    three-launch shape; the mode is read once per process."""
+    """Both 2-D halo launch shapes give the oracle's replicas for both stencils:
+    HDA_HALO_MODE=1 (pull blocks + interior + gated boundary strips in one launch) and
+    0 (comm-stream pull, interior launch, boundary launch); the default mixes them per
+    kernel.  The mode is read once per process, hence the subprocess."""
     import os
     import subprocess
     import sys
