@@ -359,6 +359,68 @@ class Gemm:
         return {"integer_exact_samples": bool((got[ii, jj].astype(np.int64) == exact).all()), "samples": 64}
 
 
+class TwoMM:
+    """the 2MM chain D = A x B ; E = C x D (16384^2 bf16
+    inputs, D bf16, E fp32) under a ROW or COL partition.  ROW re-gathers D every
+    iteration (B once); COL moves A and C once and nothing afterwards (Table 3's
+    1262.5 vs 25 GiB, P9).  One step = both products."""
+
+    def __init__(self, H, h, rank, ws, n=None, part="row"):
+        self.H, self.h, self.rank, self.ws = H, h, rank, ws
+        self.n = n or 16384
+        n = self.n
+        S = H.STAR
+        self.Ab, self.Bb, self.Cb = (synth.int_bf16(60 + i, (n, n), -1, 1) for i in range(3))
+        self.A, self.B, self.C = (h.create(H.BF16, (n, n)) for _ in range(3))
+        self.D = h.create(H.BF16, (n, n))
+        self.E = h.create(H.F32, (n, n))
+        self.part_name = part
+        self.part = h.partition(H.ROW if part == "row" else H.COL, (n, n))
+        for X, v in ((self.A, self.Ab), (self.B, self.Bb), (self.C, self.Cb)):
+            h.write(X, self.part, v)
+        self.acc1 = [(self.D, [], [(0, 0)]), (self.A, [(0, S)], []), (self.B, [(S, 0)], [])]
+        self.acc2 = [(self.E, [], [(0, 0)]), (self.C, [(0, S)], []), (self.D, [(S, 0)], [])]
+        self.kind = "2mm"
+        self.workload = (f"SURVEY 8(f)-1 2MM chain (P:L425): D=AxB, E=CxD, {n}^2 bf16 in, D bf16, E fp32, "
+                         f"{part.upper()} partition")
+        self.kname = "gemm_kernel (tcgen05), two launches per step"
+        self.dtype_name = "bf16"
+        self.metric_unit = "TFLOP/s"
+        self.flops_per_step = 4.0 * n ** 3
+        self.bound = "tensor"
+        lb, ub = h.region(self.part, rank, 2)
+        self.lb, self.ub = lb, ub
+        self.alg_per_launch = 2.0 * (ub[0] - lb[0]) * (ub[1] - lb[1]) * n
+        self.my_pts = 0
+        self.working_set = 6 * n * n * 2
+
+    def step(self):
+        self.h.apply(self.H.K_GEMM, self.part, self.acc1, [1.0, 0.0])
+        self.h.apply(self.H.K_GEMM, self.part, self.acc2, [1.0, 0.0])
+
+    def reset_input(self):
+        pass
+
+    def parity(self):
+        """D sampled against the exact integer product rounded to bf16 (RNE); E sampled
+        against the exact int64 product of C with the GPU's D (every partial sum is an
+        integer below 2^24, so fp32 accumulation is exact in any order)."""
+        D = self.h.read_replica(self.D, self.rank)
+        E = self.h.read_replica(self.E, self.rank)
+        rng = np.random.default_rng(11)
+        ii = rng.integers(self.lb[0], self.ub[0], 64)
+        jj = rng.integers(self.lb[1], self.ub[1], 64)
+        A = synth.bf16_to_f32(self.Ab[ii]).astype(np.int64)
+        exact = np.einsum("sk,ks->s", A, synth.bf16_to_f32(self.Bb[:, jj]).astype(np.int64))
+        bits = exact.astype(np.float32).view(np.uint32)
+        rne = ((bits + np.uint32(0x7FFF) + ((bits >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)).astype(np.uint16)
+        d_ok = bool((D[ii, jj] == rne).all())
+        Dv = synth.bf16_to_f32(D[:, jj]).astype(np.int64)
+        e_exact = np.einsum("sk,ks->s", synth.bf16_to_f32(self.Cb[ii]).astype(np.int64), Dv)
+        e_ok = bool((E[ii, jj].astype(np.int64) == e_exact).all())
+        return {"D_bf16_rne_exact_samples": d_ok, "E_integer_exact_samples": e_ok, "samples": 64}
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -367,7 +429,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="hdarray")
     ap.add_argument("--workload", default="jacobi2d",
-                    choices=["jacobi2d", "stencil9", "stencil7", "repartition", "gemm"])
+                    choices=["jacobi2d", "stencil9", "stencil7", "repartition", "gemm", "2mm"])
+    ap.add_argument("--part", default="row", choices=["row", "col"], help="2mm: ROW or COL partition")
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--e2e-sweeps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -377,7 +440,7 @@ def main():
     ap.add_argument("--trace", type=int, default=0, help="trace N steps after the timed region")
     args = ap.parse_args()
     defaults = {"jacobi2d": (1000, 20), "stencil9": (200, 10), "stencil7": (100, 5), "repartition": (40, 4),
-                "gemm": (20, 3)}[args.workload]
+                "gemm": (20, 3), "2mm": (10, 3)}[args.workload]
     args.steps = args.steps or defaults[0]
     args.warmup = max(args.warmup if args.warmup is not None else defaults[1], 3)
     if args.impl == "reference":
@@ -404,6 +467,8 @@ def main():
         wl = Stencil(args.workload, H, h, rank, ws, args.n)
     elif args.workload == "repartition":
         wl = Repartition(H, h, rank, ws, args.n)
+    elif args.workload == "2mm":
+        wl = TwoMM(H, h, rank, ws, args.n, args.part)
     else:
         wl = Gemm(H, h, rank, ws, args.n)
     stream = torch.cuda.ExternalStream(h.stream(rank))
@@ -475,7 +540,7 @@ def main():
     elif wl.metric_unit == "GB/s":
         value = wl.units * args.steps / (ms * 1e-3) / 1e9
     else:
-        value = 2.0 * wl.n ** 3 * args.steps / (ms * 1e-3) / 1e12
+        value = getattr(wl, "flops_per_step", 2.0 * wl.n ** 3) * args.steps / (ms * 1e-3) / 1e12
 
     # ---- per-kernel timing pass (CUDA events bracketing each launch on its stream)
     h.set_kernel_timing(True)
@@ -485,7 +550,7 @@ def main():
         wl.step()
     barrier()
     kid = {"jacobi2d": H.K_JACOBI5, "stencil9": H.K_STENCIL9, "stencil7": H.K_STENCIL7_3D,
-           "repartition": H.K_SCALE, "gemm": H.K_GEMM}[args.workload]
+           "repartition": H.K_SCALE, "gemm": H.K_GEMM, "2mm": H.K_GEMM}[args.workload]
     k_ms, k_n = h.kernel_time(kid)
     x_ms, x_n = h.exchange_time()
     st_kt = h.stats()
