@@ -577,14 +577,18 @@ def main():
                     "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": scale_bytes, "avg_launch_ms": k_avg}
     else:
-        sustained = 1399.6
+        burst, sustained = 1642.9, 1399.6
         try:
-            sustained = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"])
+            mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            burst, sustained = float(mp["bf16_tflops"]), float(mp["bf16_tflops_sustained"])
         except Exception:
             pass
+        # the tcgen05 kernel runs above cuBLAS's back-to-back "sustained" figure, so the
+        # burst figure (the larger) is the denominator; the sustained ratio rides along
         achieved = wl.alg_per_launch / (k_avg * 1e-3) / 1e12
-        roof = {"bound": "tensor", "kernel": wl.kname, "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
-                "frac": achieved / sustained, "peak_source": "measured cuBLAS bf16 sustained (MEASURED_PEAKS.json)",
+        roof = {"bound": "tensor", "kernel": wl.kname, "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
+                "frac": achieved / burst, "frac_of_sustained": achieved / sustained,
+                "peak_source": "measured cuBLAS bf16 burst (MEASURED_PEAKS.json); sustained 1399.6",
                 "algorithmic_flops_per_launch": wl.alg_per_launch, "avg_launch_ms": k_avg}
     if ws > 1:
         roof["achieved_min_over_ranks"] = -reduce(-roof["achieved"], MAX)
