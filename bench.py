@@ -493,6 +493,9 @@ def main():
     l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
     flush = wl.working_set < 2 * l2_bytes
     flush_buf = torch.empty(int(2 * l2_bytes), dtype=torch.uint8, device="cuda") if flush else None
+    # after writing the flush buffer, READ a second one of 2x L2: the flush's dirty lines
+    # are written back here, outside the timed step, instead of inside the next kernel
+    flush_rd = torch.zeros(int(2 * l2_bytes) // 8, dtype=torch.int64, device="cuda") if flush else None
 
     for _ in range(args.warmup):
         wl.step()
@@ -523,6 +526,7 @@ def main():
         for i in range(args.steps):
             with torch.cuda.stream(stream):
                 flush_buf.zero_()
+                flush_rd.max()
             if ws > 1:
                 torch.cuda.synchronize()
                 dist.barrier()
@@ -658,7 +662,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype_name, "data": "synthetic",
             "config": {"workload": wl.workload, "n": wl.n, "parallelism": f"spmd{ws}" if ws > 1 else "single",
                        "transport": ["fused", "staged", "auto"][args.transport], "overlap": not args.no_overlap,
-                       "l2": ("L2 flushed between timed steps" if flush else
+                       "l2": ("L2 flushed between timed steps (write a 2x-L2 buffer, then read another)" if flush else
                               f"inputs larger than L2 (per-GPU working set {wl.working_set / 2**20:.0f} MiB)")},
             "roofline": roof,
             "exchange": {"bytes_per_step": halo_bytes, "exchange_ms_per_step": x_avg if x_n else 0.0,
