@@ -291,42 +291,13 @@ __device__ __forceinline__ double quarter(double x) { return x * 0.25; }
 template <>
 __device__ __forceinline__ float quarter(float x) { return x * 0.25f; }
 
-// Correctly rounded x / d for a constant d without the IEEE division sequence:
-// q0 = RN(x*y) with y = RN(1/d) is faithful, the residual x - q0*d is exact (FMA), and
-// one FMA correction gives RN(x/d) (Markstein).  tools/markstein_check.c verifies it
-// exhaustively for fp32 / 6 and on 2e8 samples over every normal exponent for
-// fp64 / 20.  Zero residual returns q0 (keeps the sign of zero); non-finite and tiny
-// |x| (subnormal quotients) take the true division, a branch never taken on stencil
-// data.  Saves the MUFU + Newton + slow-path check of each division (the 9-point and
-// 3-D kernels are partly issue-bound: ncu issue-active 67% / 51%).
-__device__ __forceinline__ double div_const(double x, double d, double y) {
-  if (!(fabs(x) >= 0x1p-1000) || !(fabs(x) <= 0x1p+1000)) return x / d;
-  const double q0 = __dmul_rn(x, y);
-  const double r = __fma_rn(-q0, d, x);
-  return r == 0.0 ? q0 : __fma_rn(r, y, q0);
-}
-__device__ __forceinline__ float div_const(float x, float d, float y) {
-  if (!(fabsf(x) >= 0x1p-100f) || !(fabsf(x) <= 0x1p+100f)) return x / d;
-  const float q0 = __fmul_rn(x, y);
-  const float r = __fmaf_rn(-q0, d, x);
-  return r == 0.0f ? q0 : __fmaf_rn(r, y, q0);
-}
-template <typename T>
-__device__ __forceinline__ T div20(T x) {
-  return div_const(x, T(20), T(1) / T(20));
-}
-template <typename T>
-__device__ __forceinline__ T div6(T x) {
-  return div_const(x, T(6), T(1) / T(6));
-}
-
 template <typename T>
 __device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
   T a = ((w + e) + n) + s;
   T c = ((nw + ne) + sw) + se;
   T t = T(4) * a;
   t = t + c;
-  return div20(t);
+  return t / T(20);
 }
 
 // KIND 0 = JACOBI5, 1 = STENCIL9
@@ -792,7 +763,7 @@ __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ 
         s = s + yp[v];
         s = s + zm[r][v];
         s = s + zp[r][v];
-        o[v] = div6(s);
+        o[v] = s / T(6);
       }
       if (live && y < y1) {
         T* dst = out + z * pl + y * n2 + x;
@@ -832,7 +803,7 @@ __global__ void stencil7_scalar_kernel(const T* __restrict__ in, T* __restrict__
     s = s + p[n2];
     s = s + p[-pl];
     s = s + p[pl];
-    out[z * pl + y * n2 + x] = div6(s);
+    out[z * pl + y * n2 + x] = s / T(6);
   }
   ks_post(ks);
 }
