@@ -45,6 +45,7 @@ namespace {
 constexpr int SW_PROD = 0, SW_PACK = 64, SW_ACK = 128, SW_CTR_PULL = 192, SW_CTR_KERN = 193;
 constexpr int SW_PULLDONE = 194;  // local: epoch of the last completed overlapped pull
 constexpr int SW_RED = 256, SW_REDSIG = 320;  // reduce partials [P] and their epochs [P]
+constexpr int SW_DEBUG = 195;                  // measurement hooks only
 constexpr int SW_SCRATCH = 384;               // kReduceBlocks partials
 constexpr int SW_WORDS = SW_SCRATCH + kReduceBlocks;
 constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
@@ -962,6 +963,10 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
       if (defines) {
         war_waits(ctx, ci, q, ks);
         signal_prod(ctx, q, k, ks);
+        // HDA_DEBUG_FAKE_SIGNAL=1: a kernel with no peer to signal still runs the
+        // end-of-kernel fence + counter + store (to a local word) — measures their cost
+        static const int fake_sig = env_int("HDA_DEBUG_FAKE_SIGNAL", 0);
+        if (fake_sig && ks.nsig == 0) ks_sig(ks, ctx->dev[q].sync + SW_DEBUG);
       }
       const int X0 = ci.param_array[0];
       const TArray& a0 = ctx->tr->array(X0);
