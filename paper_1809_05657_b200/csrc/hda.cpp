@@ -968,6 +968,18 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         static const int fake_sig = env_int("HDA_DEBUG_FAKE_SIGNAL", 0);
         if (fake_sig && ks.nsig == 0) ks_sig(ks, ctx->dev[q].sync + SW_DEBUG);
       }
+      // user kernels publish PROD from a trailing signal launch (HDA_SIG_KERNEL=0: from
+      // the kernel's last CTA, after a fence in every CTA)
+      static const int sig_kernel = env_int("HDA_SIG_KERNEL", 1);
+      SignalList post_sig;
+      post_sig.n = 0;
+      const bool split_sig = sig_kernel && kern && !io && ks.nsig > 0;
+      if (split_sig) {
+        for (int i = 0; i < ks.nsig; i++) post_sig.ptr[i] = ks.sig_ptr[i];
+        post_sig.n = ks.nsig;
+        post_sig.val = ks.sig_val;
+        ks.nsig = 0;
+      }
       const int X0 = ci.param_array[0];
       const TArray& a0 = ctx->tr->array(X0);
       if (io) {
@@ -1084,6 +1096,10 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         if ((rc = timed_end(ctx, stream_of(ctx, q), kernel, a))) return rc;
       } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
         return rc;
+      }
+      if (split_sig) {
+        CK(launch_signal_pdl(post_sig, ks.relaxed, stream_of(ctx, q)));
+        count_launch(ctx);
       }
     }
   }

@@ -279,6 +279,27 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cud
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// PROD signals of a user kernel as their own tiny launch (PDL): the wait returns when
+// the kernel before it on the stream has completed — all of its writes are in this
+// GPU's L2, where peers read them — so no CTA of the big kernel pays a fence + counter
+// at its end (measured: 1.5 us/step for a one-wave share, 8 us for 8192^2 N=1 tiles).
+__global__ void signal_pdl_kernel(const __grid_constant__ SignalList l, int relaxed) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __threadfence();
+  const int i = threadIdx.x;
+  if (i < l.n) {
+    if (relaxed)
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(l.ptr[i]), "l"(l.val) : "memory");
+    else
+      st_release_sys(l.ptr[i], l.val);
+  }
+}
+cudaError_t launch_signal_pdl(const SignalList& l, int relaxed, cudaStream_t s) {
+  if (l.n <= 0) return cudaSuccess;
+  return launch_pdl(signal_pdl_kernel, dim3(1), dim3(kMaxDev), s, l, relaxed);
+}
+
 constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
 constexpr int ST_ROWS = 16;      // rows per block

@@ -76,6 +76,8 @@ struct BoxList {  // boxes in element coordinates of a 3-D padded shape
 cudaError_t launch_copy_runs(const RunBatch& b, const KSync& ks, cudaStream_t s);
 cudaError_t launch_wait(const WaitList& w, int* err_flag, long long timeout_ns, cudaStream_t s);
 cudaError_t launch_signal(const SignalList& l, cudaStream_t s);
+// after the previous kernel on s completes (programmatic dependent launch)
+cudaError_t launch_signal_pdl(const SignalList& l, int relaxed, cudaStream_t s);
 
 // user kernels over the work box [lb, ub) of one device's replica (padded 3-D shape)
 // 2-D stencils over nb (<= 8) boxes in ONE launch (lbs[i], ubs[i] front-padded 3-D)
