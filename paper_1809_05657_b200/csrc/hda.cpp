@@ -974,7 +974,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
       // sweep starts on the rows the previous one touched last (still in L2)
       static const int snake = env_int("HDA_SNAKE", 1);
       ctx->rev_now = 0;
-      if (snake && kern && kernel == KN_JACOBI5) {  // 9-point: measured slower reversed
+      if (snake && kern && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9)) {
         ctx->dev[q].dir ^= 1;
         ctx->rev_now = ctx->dev[q].dir;
       }

@@ -451,9 +451,13 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     int b;
     int64_t xb, yb;
     tile_of(bx, blockIdx.x, b, xb, yb);
-    // forward only: a second (reversed) body here cost 2.5% at N=1 (registers 44 -> 64)
-    stencil2d_body<T, KIND, ROWS, false, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                                bx.rpb[b], xb, yb);
+    if (bx.rev) {
+      stencil2d_body<T, KIND, ROWS, false, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                                 bx.rpb[b], xb, yb);
+    } else {
+      stencil2d_body<T, KIND, ROWS, false, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                                  bx.rpb[b], xb, yb);
+    }
   }
   ks_post(ks);
 }
@@ -579,8 +583,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     constexpr int ROWS = ST_ROWS;
     Boxes2 bx;
     bx.n = 0;
-    bx.rev = 0;  // the plain launch marches forward (see stencil2d_kernel)
-    (void)rev;
+    bx.rev = rev;
     for (int i = 0; i < nb && bx.n < 8; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
       if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
