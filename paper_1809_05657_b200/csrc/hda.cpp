@@ -63,7 +63,6 @@ struct Dev {
   int gpu = -1;                        // index into ctx->gpus (local devices)
   unsigned long long* sync = nullptr;  // this device's sync words (local or IPC-mapped)
   bool sync_alloc = false, sync_ipc = false;
-  int dir = 0;  // direction of this device's last 2-D stencil sweep (HDA_SNAKE)
 };
 
 struct ArrRT {
@@ -146,7 +145,6 @@ struct hda_ctx {
   std::vector<TimedEv> trace;  // kept (not drained) while tracing
   cudaEvent_t trace_ref = nullptr;
   int cur_dev = 0, cur_phase = 1;
-  int rev_now = 0;  // row-march direction of the 2-D stencil launches being issued
   std::vector<char> pulled_on_comm;  // [P] this call's pull for device q ran on the comm stream
   std::vector<const PullJob*> cur_pull;
   std::vector<const PullJob*> halo_job;  // [P] pull deferred into the fused halo-stencil launch
@@ -807,9 +805,9 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
       }
       const KSync k2 = ks_part(ctx, ks, i0 == 0, i0 + 8 >= nb);
       if (ci.kernel == KN_JACOBI5)
-        CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, lbs, ubs, n, k2, s, ctx->rev_now));
+        CK(launch_jacobi5(a0.dtype, P_(1), P_(0), S, lbs, ubs, n, k2, s));
       else
-        CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, lbs, ubs, n, k2, s, ctx->rev_now));
+        CK(launch_stencil9(a0.dtype, P_(1), P_(0), S, lbs, ubs, n, k2, s));
       count_launch(ctx);
     }
     return HDA_OK;
@@ -970,14 +968,6 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         static const int fake_sig = env_int("HDA_DEBUG_FAKE_SIGNAL", 0);
         if (fake_sig && ks.nsig == 0) ks_sig(ks, ctx->dev[q].sync + SW_DEBUG);
       }
-      // consecutive 2-D stencil sweeps on a device alternate their row direction, so a
-      // sweep starts on the rows the previous one touched last (still in L2)
-      static const int snake = env_int("HDA_SNAKE", 1);
-      ctx->rev_now = 0;
-      if (snake && kern && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9)) {
-        ctx->dev[q].dir ^= 1;
-        ctx->rev_now = ctx->dev[q].dir;
-      }
       // user kernels publish PROD from a trailing signal launch (HDA_SIG_KERNEL=0: from
       // the kernel's last CTA, after a fence in every CTA)
       static const int sig_kernel = env_int("HDA_SIG_KERNEL", 1);
@@ -1066,7 +1056,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         cudaEvent_t a;
         if ((rc = timed_begin(ctx, st, &a))) return rc;
         CK(launch_stencil2d_halo(kernel, a0.dtype, P_(1), P_(0), S, lbs, ubs, (int)fb.size(),
-                                 (int)job.interior.size(), job.batches[0], hp, ks, st, ctx->rev_now));
+                                 (int)job.interior.size(), job.batches[0], hp, ks, st));
         count_launch(ctx);
         ctx->cur_dev = q;
         ctx->cur_phase = 1;

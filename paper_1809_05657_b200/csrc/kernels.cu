@@ -330,14 +330,9 @@ struct Boxes2 {
   int64_t tstart[9];  // flat-grid launches: first tile of each box
   int32_t gx[8], gy[8];
   int32_t n;
-  int32_t rev;  // march bottom-up (alternate sweeps; see stencil2d_body)
 };
 
-// REV: march the block's rows bottom-up (virtual row v is physical row rs+re-1-v, and
-// the up/down operands swap so the arithmetic is unchanged).  Consecutive sweeps
-// alternate direction, so each sweep starts on the rows the previous one wrote last —
-// still in L2 (126 MB) — instead of the rows it wrote first.
-template <typename T, int KIND, int ROWS, bool CG, bool REV>
+template <typename T, int KIND, int ROWS, bool CG>
 __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
                                                int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase,
                                                int64_t rpb, int64_t xb, int64_t yb) {
@@ -348,7 +343,6 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
   const bool live = col < ld;
   const int64_t rs = r0 + yb * rpb;
   const int64_t re = min(rs + rpb, r1);
-  auto prow = [&](int64_t v) { return REV ? rs + re - 1 - v : v; };
   T w[W][V];
 
   auto load_row = [&](T(&r)[V], int64_t row) {
@@ -371,41 +365,38 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
     if (lane == 31 && live && col + V < ld) R = CG ? __ldcg(in + row * ld + col + V) : __ldg(in + row * ld + col + V);
   };
 
-  load_row(w[0], prow(rs - 1));
-  load_row(w[1], prow(rs));
+  load_row(w[0], rs - 1);
+  load_row(w[1], rs);
   for (int64_t base = rs; base < re; base += ST_GROUP) {
 #pragma unroll
     for (int k = 0; k < ST_GROUP; k++)
-      if (base + 1 + k <= re) load_row(w[k + 2], prow(base + 1 + k));
+      if (base + 1 + k <= re) load_row(w[k + 2], base + 1 + k);
 #pragma unroll
     for (int k = 0; k < ST_GROUP; k++) {
       const int64_t r = base + k;
       if (r >= re) break;
       T o[V];
-      const int64_t pr = prow(r);
       if (KIND == 0) {
         T L, R;
-        edges(w[k + 1], pr, L, R);
+        edges(w[k + 1], r, L, R);
 #pragma unroll
         for (int v = 0; v < V; v++) {
           const T left = v == 0 ? L : w[k + 1][v - 1];
           const T right = v == V - 1 ? R : w[k + 1][v + 1];
-          const T up = REV ? w[k + 2][v] : w[k][v];
-          const T dn = REV ? w[k][v] : w[k + 2][v];
-          o[v] = quarter<T>(((left + right) + up) + dn);
+          o[v] = quarter<T>(((left + right) + w[k][v]) + w[k + 2][v]);
         }
       } else {
         // recompute the row-edge shuffles of up/cur/dn for every output row: keeping
         // them in a register window cost occupancy (tuned: 84% vs 73% of HBM)
         T ul, ur, cl, cr, dl, dr;
-        edges(REV ? w[k + 2] : w[k], pr - 1, ul, ur);
-        edges(w[k + 1], pr, cl, cr);
-        edges(REV ? w[k] : w[k + 2], pr + 1, dl, dr);
+        edges(w[k], r - 1, ul, ur);
+        edges(w[k + 1], r, cl, cr);
+        edges(w[k + 2], r + 1, dl, dr);
 #pragma unroll
         for (int v = 0; v < V; v++) {
-          const T* up = REV ? w[k + 2] : w[k];
+          const T* up = w[k];
           const T* cu = w[k + 1];
-          const T* dn = REV ? w[k] : w[k + 2];
+          const T* dn = w[k + 2];
           const T cL = v == 0 ? cl : cu[v - 1], cR = v == V - 1 ? cr : cu[v + 1];
           const T uL = v == 0 ? ul : up[v - 1], uR = v == V - 1 ? ur : up[v + 1];
           const T dL = v == 0 ? dl : dn[v - 1], dR = v == V - 1 ? dr : dn[v + 1];
@@ -413,7 +404,7 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
         }
       }
       if (live) {
-        T* dst = out + pr * ld + col;
+        T* dst = out + r * ld + col;
         if (col >= c0 && col + V <= c1) {
           V16<T>::store(dst, o);
         } else {
@@ -438,7 +429,6 @@ __device__ __forceinline__ void tile_of(const Boxes2& bx, int64_t t, int& b, int
   const int64_t local = t - bx.tstart[b];
   xb = local % bx.gx[b];
   yb = local / bx.gx[b];
-  if (bx.rev) yb = bx.gy[b] - 1 - yb;  // bottom tiles first
 }
 
 template <typename T, int KIND, int ROWS>
@@ -451,13 +441,8 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     int b;
     int64_t xb, yb;
     tile_of(bx, blockIdx.x, b, xb, yb);
-    if (bx.rev) {
-      stencil2d_body<T, KIND, ROWS, false, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                                 bx.rpb[b], xb, yb);
-    } else {
-      stencil2d_body<T, KIND, ROWS, false, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                                  bx.rpb[b], xb, yb);
-    }
+    stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                         bx.rpb[b], xb, yb);
   }
   ks_post(ks);
 }
@@ -540,14 +525,11 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs t
       }
     }
     __syncthreads();
-    stencil2d_body<T, KIND, ROWS, true, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                               bx.rpb[b], xb, yb);
-  } else if (bx.rev) {
-    stencil2d_body<T, KIND, ROWS, false, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                               bx.rpb[b], xb, yb);
+    stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b], bx.rpb[b],
+                                        xb, yb);
   } else {
-    stencil2d_body<T, KIND, ROWS, false, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                                bx.rpb[b], xb, yb);
+    stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
+                                         bx.rpb[b], xb, yb);
   }
   ks_post(ks);
 }
@@ -573,8 +555,7 @@ __global__ void stencil2d_scalar_kernel(const T* __restrict__ in, T* __restrict_
 
 template <typename T, int KIND>
 static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape, const int64_t* const* lbs,
-                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s,
-                                      int rev) {
+                                      const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
   const int64_t ld = shape[2];
   constexpr int V = V16<T>::n;
   const bool vec = (ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
@@ -583,7 +564,6 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     constexpr int ROWS = ST_ROWS;
     Boxes2 bx;
     bx.n = 0;
-    bx.rev = rev;
     for (int i = 0; i < nb && bx.n < 8; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
       if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
@@ -644,13 +624,12 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
 template <typename T, int KIND>
 static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, const int64_t* const* lbs,
                                  const int64_t* const* ubs, int nb, int n_interior, const RunBatch& pull,
-                                 const HaloPull& hp, const KSync& ks, cudaStream_t s, int rev) {
+                                 const HaloPull& hp, const KSync& ks, cudaStream_t s) {
   const int64_t ld = shape[2];
   constexpr int V = V16<T>::n;
   constexpr int ROWS = ST_ROWS;
   Boxes2 bx;
   bx.n = 0;
-  bx.rev = rev;
   int ni = 0;
   for (int i = 0; i < nb && bx.n < 8; i++) {
     const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
@@ -716,29 +695,27 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
 
 cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
                                   const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,
-                                  const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s, int rev) {
+                                  const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s) {
   if (kernel == 1) {
     if (dtype == 0)
-      return launch_halo_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s, rev);
-    return launch_halo_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s, rev);
+      return launch_halo_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
+    return launch_halo_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
   }
   if (dtype == 0)
-    return launch_halo_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s, rev);
-  return launch_halo_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s, rev);
+    return launch_halo_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
+  return launch_halo_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, n_interior, pull, hp, ks, s);
 }
 
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
-                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s, int rev) {
-  if (dtype == 0)
-    return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s, rev);
-  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s, rev);
+                           const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+  if (dtype == 0) return launch_stencil2d_t<double, 0>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
+  return launch_stencil2d_t<float, 0>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
 }
 
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape, const int64_t* const* lbs,
-                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s, int rev) {
-  if (dtype == 0)
-    return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s, rev);
-  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s, rev);
+                            const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
+  if (dtype == 0) return launch_stencil2d_t<double, 1>((const double*)in, (double*)out, shape, lbs, ubs, nb, ks, s);
+  return launch_stencil2d_t<float, 1>((const float*)in, (float*)out, shape, lbs, ubs, nb, ks, s);
 }
 
 // =====================================================================================

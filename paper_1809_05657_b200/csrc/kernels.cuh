@@ -96,15 +96,14 @@ struct HaloPull {
 };
 cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
                                   const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,
-                                  const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s, int rev = 0);
+                                  const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s);
 // up to 8 boxes in one launch (flat grid of tiles)
-// rev = 1: rows marched bottom-up (alternating sweeps reuse the rows still in L2)
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
                            const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
-                           cudaStream_t s, int rev = 0);
+                           cudaStream_t s);
 cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,
-                            cudaStream_t s, int rev = 0);
+                            cudaStream_t s);
 cudaError_t launch_stencil7(int dtype, const void* in, void* out, const int64_t* shape,
                             const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
 cudaError_t launch_scale(int dtype, void* x, const int64_t* shape, const int64_t* lb,
