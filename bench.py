@@ -130,9 +130,18 @@ def oracle_sample(seconds_target=15.0, rows=1026, cols=8192, max_sweeps=400):
             "sample": f"oracle P=1 Jacobi on a {rows}x{cols} slab of configs[1], {s} sweeps, {dt:.1f} s"}
 
 
+def jacobi_workload(n):
+    return (f"configs[1]: {n}x{n} fp64 Jacobi (P:L459), ROW partition of the interior, "
+            "ping-pong sweeps through hda_apply")
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
+        return 0
+    if args.workload != "jacobi2d":
+        print(json.dumps({"impl": "reference", "unavailable": "the oracle arm times the default jacobi2d workload "
+                                                              "only"}), flush=True)
         return 0
     import oracle as O
     import synth
@@ -156,9 +165,11 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "configs[1] 8192^2 fp64 Jacobi (bounded sample: 258x8192 slab per step)"},
+            "config": {"workload": jacobi_workload(8192), "n": 8192,
+                       "parallelism": f"spmd{ws}" if ws > 1 else "single"},
             "cpu_baseline": {"value": v, "unit": "GPoints/s", "cores": 1, "kind": "oracle",
-                             "sample": f"oracle P=1 Jacobi sweep of a {rows}x{cols} slab per step"},
+                             "sample": f"oracle (plain C, one thread, rank 0 only) P=1 Jacobi sweep of a {rows}x{cols} "
+                                       "slab of configs[1] per step; value = slab points / time"},
             "e2e": {"value": v, "unit": "GPoints/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -180,8 +191,7 @@ class Stencil:
             self.shape, self.dt, self.es = (self.n, self.n), H.F64, 8
             self.K, self.uses, self.part_kind = H.K_JACOBI5, J, H.ROW
             self.modes = (37, 61)
-            self.workload = (f"configs[1]: {self.n}x{self.n} fp64 Jacobi (P:L459), ROW partition of the interior, "
-                             "ping-pong sweeps through hda_apply")
+            self.workload = jacobi_workload(self.n)
             self.kname = "stencil2d_kernel<double,JACOBI5>"
         elif kind == "stencil9":
             self.n = n or 16384
