@@ -347,6 +347,88 @@ __global__ void __launch_bounds__(256, MINB) march9h(const double* __restrict__ 
   }
 }
 
+// rec1 with a check-free body for full tiles (all columns live and inside [c0,c1),
+// ROWS complete rows): no per-row bounds tests, unconditional vector stores and edge
+// loads; the general body handles the ragged blocks.
+template <int ROWS, int GROUP, bool FULL>
+__device__ __forceinline__ void body9(const double* __restrict__ in, double* __restrict__ out, long ld, long rs,
+                                      long re, long c0, long c1, long col, int lane) {
+  constexpr int W = GROUP + 2;
+  const bool live = FULL || col < ld;
+  double w[W][2];
+  auto ldr = [&](double(&r)[2], long row) {
+    if (live) {
+      double2 v = __ldg(reinterpret_cast<const double2*>(in + row * ld + col));
+      r[0] = v.x;
+      r[1] = v.y;
+    } else {
+      r[0] = r[1] = 0;
+    }
+  };
+  auto edges = [&](const double(&r)[2], long row, double& L, double& R) {
+    L = __shfl_up_sync(0xffffffffu, r[1], 1);
+    R = __shfl_down_sync(0xffffffffu, r[0], 1);
+    if (FULL) {
+      if (lane == 0) L = __ldg(in + row * ld + col - 1);
+      if (lane == 31) R = __ldg(in + row * ld + col + 2);
+    } else {
+      if (lane == 0 && live && col > 0) L = __ldg(in + row * ld + col - 1);
+      if (lane == 31 && live && col + 2 < ld) R = __ldg(in + row * ld + col + 2);
+    }
+  };
+  ldr(w[0], rs - 1);
+  ldr(w[1], rs);
+  for (long base = rs; base < re; base += GROUP) {
+#pragma unroll
+    for (int k = 0; k < GROUP; k++)
+      if (FULL || base + 1 + k <= re) ldr(w[k + 2], base + 1 + k);
+#pragma unroll
+    for (int k = 0; k < GROUP; k++) {
+      const long r = base + k;
+      if (!FULL && r >= re) break;
+      double ul, ur, cl, cr, dl, dr;
+      edges(w[k], r - 1, ul, ur);
+      edges(w[k + 1], r, cl, cr);
+      edges(w[k + 2], r + 1, dl, dr);
+      const double* up = w[k];
+      const double* cu = w[k + 1];
+      const double* dn = w[k + 2];
+      double o0 = st9(cl, cu[1], up[0], dn[0], ul, up[1], dl, dn[1]);
+      double o1 = st9(cu[0], cr, up[1], dn[1], up[0], ur, dn[0], dr);
+      double* d = out + r * ld + col;
+      if (FULL) {
+        *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+      } else if (live) {
+        if (col >= c0 && col + 2 <= c1)
+          *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+        else {
+          if (col >= c0 && col < c1) d[0] = o0;
+          if (col + 1 >= c0 && col + 1 < c1) d[1] = o1;
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 2; v++) {
+      w[0][v] = w[GROUP][v];
+      w[1][v] = w[GROUP + 1][v];
+    }
+  }
+}
+template <int ROWS, int GROUP, int MINB>
+__global__ void __launch_bounds__(256, MINB) march9f(const double* __restrict__ in, double* __restrict__ out, long ld,
+                                                     long r0, long r1, long c0, long c1, long cbase) {
+  const int lane = threadIdx.x & 31;
+  const long col = cbase + ((long)blockIdx.x * 256 + threadIdx.x) * 2;
+  const long rs = r0 + (long)blockIdx.y * ROWS;
+  const long re = min(rs + (long)ROWS, r1);
+  const long bc0 = cbase + (long)blockIdx.x * 512;  // block-uniform column range
+  const bool full = bc0 >= c0 && bc0 >= 1 && bc0 + 512 <= c1 && bc0 + 512 + 1 <= ld && re - rs == ROWS;
+  if (full)
+    body9<ROWS, GROUP, true>(in, out, ld, rs, re, c0, c1, col, lane);
+  else
+    body9<ROWS, GROUP, false>(in, out, ld, rs, re, c0, c1, col, lane);
+}
+
 int main() {
   const long n = 8192;
   const size_t bytes = n * n * 8;
@@ -416,11 +498,16 @@ int main() {
     march9h<ROWS, G, MINB><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);                         \
   })
   M9H(16, 4, 4);
-  M9H(16, 4, 5);
-  M9H(16, 2, 5);
-  M9H(16, 4, 6);
-  M9H(32, 4, 5);
-  M9H(16, 8, 4);
+#define M9F(ROWS, G, MINB)                                                                     \
+  time_it("st9f R" #ROWS " G" #G " minB" #MINB, [&] {                                           \
+    dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));      \
+    march9f<ROWS, G, MINB><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);                         \
+  })
+  M9F(16, 4, 5);
+  M9F(16, 4, 4);
+  M9F(32, 4, 5);
+  M9F(16, 2, 5);
+  M9F(16, 2, 6);
   // plain copy for reference bandwidth
   {
     cudaEventRecord(a);
