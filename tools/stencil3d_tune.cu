@@ -192,6 +192,84 @@ __global__ void __launch_bounds__(256, MINB) k_rows(const float* __restrict__ in
   }
 }
 
+// "rows" + software pipelining: the loads of plane z+1's y halos and of plane z+2 are
+// issued one iteration ahead, so each iteration's arithmetic overlaps the next loads.
+template <int R, int ZCH, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_rowsp(const float* __restrict__ in, float* __restrict__ out, long n1,
+                                                     long n2, long z0, long z1, long y0, long y1, long x0, long x1) {
+  const int lane = threadIdx.x & 31;
+  const long x = ((long)blockIdx.x * 256 + threadIdx.x) * 4;
+  const long ya = y0 + (long)blockIdx.y * R;
+  const bool live = x < n2;
+  const long zs = z0 + (long)blockIdx.z * ZCH, ze = min(zs + (long)ZCH, z1);
+  const long pl = n1 * n2;
+  auto ld = [&](long z, long yy) -> float4 {
+    return (live && yy < n1) ? __ldg(reinterpret_cast<const float4*>(in + z * pl + yy * n2 + x))
+                             : make_float4(0, 0, 0, 0);
+  };
+  float4 zm[R], zc[R], zp[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    zm[r] = ld(zs - 1, ya + r);
+    zc[r] = ld(zs, ya + r);
+    zp[r] = ld(zs + 1, ya + r);
+  }
+  float4 top = ld(zs, ya - 1), bot = ld(zs, ya + R);
+  for (long z = zs; z < ze; z++) {
+    // next iteration's loads first
+    float4 zn[R], topn, botn;
+    const bool more = z + 1 < ze;
+    if (more) {
+#pragma unroll
+      for (int r = 0; r < R; r++) zn[r] = ld(z + 2, ya + r);
+      topn = ld(z + 1, ya - 1);
+      botn = ld(z + 1, ya + R);
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const long y = ya + r;
+      const float4 c = zc[r];
+      const float4 ym = r == 0 ? top : zc[r - 1];
+      const float4 yp = r == R - 1 ? bot : zc[r + 1];
+      float L = __shfl_up_sync(0xffffffffu, c.w, 1);
+      float Rr = __shfl_down_sync(0xffffffffu, c.x, 1);
+      const float* row = in + z * pl + y * n2 + x;
+      if (lane == 0 && live && x > 0 && y < y1) L = __ldg(row - 1);
+      if (lane == 31 && live && x + 4 < n2 && y < y1) Rr = __ldg(row + 4);
+      const float cc[4] = {c.x, c.y, c.z, c.w}, m[4] = {ym.x, ym.y, ym.z, ym.w}, p[4] = {yp.x, yp.y, yp.z, yp.w},
+                  a[4] = {zm[r].x, zm[r].y, zm[r].z, zm[r].w}, b[4] = {zp[r].x, zp[r].y, zp[r].z, zp[r].w};
+      float o[4];
+#pragma unroll
+      for (int v = 0; v < 4; v++) {
+        float s = (v == 0 ? L : cc[v - 1]) + (v == 3 ? Rr : cc[v + 1]);
+        s = s + m[v];
+        s = s + p[v];
+        s = s + a[v];
+        s = s + b[v];
+        o[v] = s / 6.0f;
+      }
+      if (live && y < y1) {
+        float* d = out + z * pl + y * n2 + x;
+        if (x >= x0 && x + 4 <= x1)
+          *reinterpret_cast<float4*>(d) = make_float4(o[0], o[1], o[2], o[3]);
+        else
+          for (int v = 0; v < 4; v++)
+            if (x + v >= x0 && x + v < x1) d[v] = o[v];
+      }
+    }
+    if (more) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        zm[r] = zc[r];
+        zc[r] = zp[r];
+        zp[r] = zn[r];
+      }
+      top = topn;
+      bot = botn;
+    }
+  }
+}
+
 // shared-memory plane tiles: the block's (BY+2) rows of plane z are staged in smem
 // (double-buffered, one barrier per plane); y neighbours come from smem
 template <int BY, int ZCH>
@@ -322,6 +400,16 @@ int main() {
   ROWSV(4, 64, 3);
   ROWSV(8, 64, 2);
   ROWSV(2, 64, 4);
+#define ROWSP(R, ZCH, MINB)                                                                              \
+  time_it("rowsp R" #R " Z" #ZCH " minB" #MINB, [&] {                                                   \
+    dim3 g((unsigned)((n + 1023) / 1024), (unsigned)((hi - lo + R - 1) / R), (unsigned)((hi - lo + ZCH - 1) / ZCH)); \
+    k_rowsp<R, ZCH, MINB><<<g, 256>>>(X, Y, n, n, lo, hi, lo, hi, lo, hi);                                \
+  }, false)
+  ROWSP(1, 32, 4);
+  ROWSP(2, 32, 4);
+  ROWSP(2, 32, 3);
+  ROWSP(1, 64, 5);
+  ROWSP(2, 16, 4);
 #define SMEM(BY, ZCH)                                                                                     \
   time_it("smem BY" #BY " Z" #ZCH, [&] {                                                                 \
     dim3 g((unsigned)((n + 127) / 128), (unsigned)((hi - lo + BY - 1) / BY), (unsigned)((hi - lo + ZCH - 1) / ZCH)); \
