@@ -441,7 +441,10 @@ def main():
     ap.add_argument("--workload", default="jacobi2d",
                     choices=["jacobi2d", "stencil9", "stencil7", "repartition", "gemm", "2mm"])
     ap.add_argument("--part", default="row", choices=["row", "col"], help="2mm: ROW or COL partition")
-    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--size", "--n", dest="n", type=int, default=None,
+                    help="problem edge (use --size under torchrun: its parser takes --n as its own prefix)")
+    ap.add_argument("--watchdog", type=float, default=0.0,
+                    help="dump every thread's Python stack and exit after this many seconds (debugging hangs)")
     ap.add_argument("--e2e-sweeps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -449,6 +452,9 @@ def main():
     ap.add_argument("--no-overlap", action="store_true")
     ap.add_argument("--trace", type=int, default=0, help="trace N steps after the timed region")
     args = ap.parse_args()
+    if args.watchdog > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.watchdog, exit=True)
     defaults = {"jacobi2d": (1000, 20), "stencil9": (200, 10), "stencil7": (100, 5), "repartition": (40, 4),
                 "gemm": (20, 3), "2mm": (10, 3)}[args.workload]
     args.steps = args.steps or defaults[0]

@@ -17,7 +17,7 @@ for n in 2 $NG; do
       > gpurun_out/${TAG}_${w}_n$n.json 2>/dev/null
   done
 done
-timeout 600 $TR --nproc-per-node $NG bench.py --gpus $NG --n 5792 --no-cpu-baseline > gpurun_out/${TAG}_jacobi5792_flush_n$NG.json 2>/dev/null
+timeout 600 $TR --nproc-per-node $NG bench.py --gpus $NG --size 5792 --no-cpu-baseline > gpurun_out/${TAG}_jacobi5792_flush_n$NG.json 2>/dev/null
 timeout 600 $TR --nproc-per-node $NG bench.py --gpus $NG --impl reference > gpurun_out/${TAG}_reference_n$NG.json 2>/dev/null
 for f in gpurun_out/${TAG}_*.json; do
   printf "%-40s " $(basename $f)
