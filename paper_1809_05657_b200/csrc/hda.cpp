@@ -1141,6 +1141,9 @@ static hda_ctx_t* new_ctx(int P) {
   ctx->pulled_on_comm.assign(P, 0);
   ctx->cur_pull.assign(P, nullptr);
   ctx->halo_job.assign(P, nullptr);
+  // HDA_TIMEOUT_MS: bound on every cross-device wait (default 60 s); a short value
+  // turns a protocol deadlock into a prompt HDA_ETIMEOUT when debugging
+  if (int ms = env_int("HDA_TIMEOUT_MS", 0)) ctx->timeout_ns = 1000000LL * ms;
   return ctx;
 }
 
