@@ -25,6 +25,7 @@ def _port():
 
 def _worker(rank, world, port, q, env1):
     try:
+        os.environ["HDA_TIMEOUT_MS"] = "20000"  # a protocol deadlock fails in seconds
         if rank == 1:  # rank 1 only: an asymmetric slow reader opens the WAR window
             os.environ.update(env1)
         import torch
@@ -86,6 +87,19 @@ def _worker(rank, world, port, q, env1):
                 be.apply(H.K_SCALE, cp, [(Z, [(0, 0)], [(0, 0)])], [2.0])
                 be.apply(H.K_SCALE, rp, [(Z, [(0, 0)], [(0, 0)])], [0.5])
         check("bulk", [Z])
+        # GPU-filling in-place SCALE kernels whose WAR waits depend on the peer's bulk
+        # copy-engine pulls: waiting inside every CTA starved the copies (deadlock,
+        # found in the configs[3] bench); the wait now runs in one CTA first
+        big2 = (4096, 4096)
+        for be in (h, w):
+            Z2 = be.create(H.F32, big2)
+            rp2 = be.partition(H.ROW, big2)
+            cp2 = be.partition(H.COL, big2)
+            be.apply(H.K_STAMP, rp2, [(Z2, [], [(0, 0)])], [4242.0])
+            for it in range(2):
+                be.apply(H.K_SCALE, cp2, [(Z2, [(0, 0)], [(0, 0)])], [2.0])
+                be.apply(H.K_SCALE, rp2, [(Z2, [(0, 0)], [(0, 0)])], [0.5])
+        check("bulk-gpu-filling", [Z2])
         # Reduce over NVLink sync words: every rank gets the oracle's value
         ints = np.arange(np.prod(shape), dtype=np.float64).reshape(shape) % 97
         for be in (h, w):
