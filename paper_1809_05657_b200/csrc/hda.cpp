@@ -1067,12 +1067,12 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         Gpu& g = ctx->gpus[ctx->dev[q].gpu];
         bool joined = false;
         const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
-        if (!job.ce.empty() && ks.nwait > 0) {
-          // The peers' bulk copies this WAR wait depends on may need SM time on their
-          // GPUs (measured: cross-process 3-D peer copies stall behind a GPU-filling
-          // kernel); if every CTA of the interior spun here while the peers did the
-          // same, neither GPU would free the SMs the other's copy needs.  Wait in one
-          // CTA, then launch the interior with no waits.
+        if (ks.nwait > 0) {
+          // The peers' pulls this WAR wait depends on need SM time (their pull kernels)
+          // or stall behind GPU-filling kernels (measured: cross-process 3-D peer copies
+          // on the copy engine); if every CTA of the interior spun here while the peers
+          // did the same, neither GPU would free what the other's pull needs.  Wait in
+          // one CTA, then launch the interior with no waits.
           KSync w = ks_empty(ctx);
           std::memcpy(w.wait_ptr, ks.wait_ptr, sizeof w.wait_ptr);
           std::memcpy(w.wait_val, ks.wait_val, sizeof w.wait_val);
