@@ -493,3 +493,40 @@ def test_trace_rows(H):
     assert (t[:, 4] >= t[:, 3]).all() and (t[:, 3] >= 0).all()
     assert set(t[:, 1].astype(int)) == {0, 1}
     h.close()
+
+
+# ------------------------------------------------------------------ frontend (§8(f)-4)
+def test_frontend_program_on_gpu(H):
+    """config 1 driven through `#pragma hdarray` sources and file M on the GPU: every
+    replica bit-exact with the oracle's explicit-offset run."""
+    from paper_1809_05657_b200 import frontend as F
+    src = r"""
+#pragma hdarray use(B,(0,-1)) use(B,(0,1)) use(B,(-1,0)) use(B,(1,0)) def(A,(0,0))
+__global__ void jacobi_step(double *A, const double *B) { }
+#pragma hdarray use(A,(0,0)) def(B,(0,0))
+__global__ void copy_back(double *B, const double *A) { }
+"""
+    n, P = 16, 4
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    prog = F.Program(h, F.parse(src))
+    prog.bind("jacobi_step", H.K_JACOBI5, arrays=["A", "B"])
+    prog.bind("copy_back", H.K_COPY, arrays=["B", "A"])
+    w = O.Oracle(P)
+    ia, ib = synth.uniform(21, (n, n)), synth.uniform(22, (n, n))
+    hs = {}
+    for be in (h, w):
+        A, B = be.create(H.F64, (n, n)), be.create(H.F64, (n, n))
+        data = be.partition(H.ROW, (n, n))
+        work = be.partition(H.ROW, (n, n), (1, 1), (n - 1, n - 1))
+        be.write(A, data, ia)
+        be.write(B, data, ib)
+        hs[be] = (A, B, work)
+    A, B, work = hs[h]
+    Aw, Bw, workw = hs[w]
+    for s in range(3):
+        prog.apply_kernel("jacobi_step", work, A, B)
+        prog.apply_kernel("copy_back", work, B, A)
+        w.apply(O.K_JACOBI5, workw, [(Aw, [], [(0, 0)]), (Bw, J, [])])
+        w.apply(O.K_COPY, workw, [(Bw, [], [(0, 0)]), (Aw, [(0, 0)], [])])
+    assert_replicas(h, w, [A, B], P)
+    h.close()
