@@ -524,8 +524,23 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs t
       }
     }
     __syncthreads();
-    stencil2d_body<T, KIND, ROWS, true>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b], bx.rpb[b],
-                                        xb, yb);
+    // boundary strips are thin (a row or a column): one point per thread with
+    // L1-bypassing loads, instead of a second (cache-global) copy of the register-window
+    // body that pushed the 9-point kernel into spills
+    const int64_t rs = bx.r0[b] + yb * bx.rpb[b], re = min(rs + bx.rpb[b], bx.r1[b]);
+    const int64_t cs = max(bx.c0[b], bx.cbase[b] + xb * ST_THREADS * V16<T>::n);
+    const int64_t ce = min(bx.c1[b], bx.cbase[b] + (xb + 1) * ST_THREADS * V16<T>::n);
+    const int64_t w = ce - cs;
+    for (int64_t i = threadIdx.x; w > 0 && i < (re - rs) * w; i += ST_THREADS) {
+      const int64_t r = rs + i / w, c = cs + i % w;
+      const T* p = in + r * ld + c;
+      if (KIND == 0) {
+        out[r * ld + c] = quarter<T>(((__ldcg(p - 1) + __ldcg(p + 1)) + __ldcg(p - ld)) + __ldcg(p + ld));
+      } else {
+        out[r * ld + c] = st9<T>(__ldcg(p - 1), __ldcg(p + 1), __ldcg(p - ld), __ldcg(p + ld), __ldcg(p - ld - 1),
+                                 __ldcg(p - ld + 1), __ldcg(p + ld - 1), __ldcg(p + ld + 1));
+      }
+    }
   } else {
     stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
                                          bx.rpb[b], xb, yb);
