@@ -591,7 +591,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
     }
     // Large boxes: 16-row tiles, many waves (94% of HBM at 8190 rows).  Boxes that
-    // would take fewer than ~8 waves (a GPU's share at N >= 4) instead get one wave of
+    // would take fewer than ~5 waves (a GPU's share at N >= 4) instead get one wave of
     // 148 x ST_MINB blocks marching contiguous row ranges: no tail wave, 2 halo rows
     // per block, and register headroom on every SM for an overlapped halo pull.
     // Narrow boxes (column strips of a BLOCK halo: one live thread per block) keep
@@ -602,7 +602,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
     }
     const int64_t wave = (int64_t)sm_count_dev() * ST_MINB;
-    const bool one_wave = one_wave_enabled() && tiles16 < 8 * wave;
+    const bool one_wave = one_wave_enabled() && tiles16 < 5 * wave;
     bx.tstart[0] = 0;
     for (int k = 0; k < bx.n; k++) {
       const int64_t rows = bx.r1[k] - bx.r0[k];
@@ -660,7 +660,7 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
   }
   int64_t pb = (pull.total_units + 7) / 8;  // 8 warps per block
   const int npull = (int)std::max<int64_t>(1, std::min<int64_t>(pb, 64));
-  // Interior boxes: when the GPU's share is under ~8 waves of 16-row tiles, ONE wave
+  // Interior boxes: when the GPU's share is under ~5 waves of 16-row tiles, ONE wave
   // of row-range blocks sized to the slots the pull blocks leave free (blocks that
   // miss the first wave would double the step); the boundary strips keep 16-row tiles
   // and run in the slots the pull blocks vacate.
@@ -675,7 +675,7 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
     if (k < ni && bx.c1[k] - bx.c0[k] > 64) strips_i += bx.gx[k];
   }
-  const bool one_wave = one_wave_enabled() && tiles16 < 8 * wave && strips_i > 0 && wave - npull >= strips_i;
+  const bool one_wave = one_wave_enabled() && tiles16 < 5 * wave && strips_i > 0 && wave - npull >= strips_i;
   bx.tstart[0] = 0;
   for (int k = 0; k < bx.n; k++) {
     const int64_t rows = bx.r1[k] - bx.r0[k];
