@@ -429,6 +429,74 @@ __global__ void __launch_bounds__(256, MINB) march9f(const double* __restrict__ 
     body9<ROWS, GROUP, false>(in, out, ld, rs, re, c0, c1, col, lane);
 }
 
+// rec1 with strength-reduced addressing: running row pointers (no 64-bit row*ld per
+// load), edge predicates hoisted out of the row loop
+template <int ROWS, int GROUP, int MINB>
+__global__ void __launch_bounds__(256, MINB) march9q(const double* __restrict__ in, double* __restrict__ out, long ld,
+                                                     long r0, long r1, long c0, long c1, long cbase) {
+  constexpr int W = GROUP + 2;
+  const int lane = threadIdx.x & 31;
+  const long col = cbase + ((long)blockIdx.x * 256 + threadIdx.x) * 2;
+  const bool live = col < ld;
+  const long rs = r0 + (long)blockIdx.y * ROWS;
+  const long re = min(rs + (long)ROWS, r1);
+  const bool ledge = lane == 0 && live && col > 0;
+  const bool redge = lane == 31 && live && col + 2 < ld;
+  const bool full_store = live && col >= c0 && col + 2 <= c1;
+  const double* p = in + (rs - 1) * ld + col;  // row rs-1
+  double* q = out + rs * ld + col;
+  double w[W][2];
+  auto ldr = [&](double(&r)[2], const double* a) {
+    if (live) {
+      double2 v = __ldg(reinterpret_cast<const double2*>(a));
+      r[0] = v.x;
+      r[1] = v.y;
+    } else {
+      r[0] = r[1] = 0;
+    }
+  };
+  auto edges = [&](const double(&r)[2], const double* a, double& L, double& R) {
+    L = __shfl_up_sync(0xffffffffu, r[1], 1);
+    R = __shfl_down_sync(0xffffffffu, r[0], 1);
+    if (ledge) L = __ldg(a - 1);
+    if (redge) R = __ldg(a + 2);
+  };
+  ldr(w[0], p);
+  ldr(w[1], p + ld);
+  for (long base = rs; base < re; base += GROUP) {
+    const double* pb = p + (base - rs + 2) * ld;  // row base+1
+#pragma unroll
+    for (int k = 0; k < GROUP; k++)
+      if (base + 1 + k <= re) ldr(w[k + 2], pb + k * ld);
+#pragma unroll
+    for (int k = 0; k < GROUP; k++) {
+      if (base + k >= re) break;
+      const double* pr = pb + (k - 1) * ld;  // row base+k
+      double ul, ur, cl, cr, dl, dr;
+      edges(w[k], pr - ld, ul, ur);
+      edges(w[k + 1], pr, cl, cr);
+      edges(w[k + 2], pr + ld, dl, dr);
+      const double* up = w[k];
+      const double* cu = w[k + 1];
+      const double* dn = w[k + 2];
+      double o0 = st9(cl, cu[1], up[0], dn[0], ul, up[1], dl, dn[1]);
+      double o1 = st9(cu[0], cr, up[1], dn[1], up[0], ur, dn[0], dr);
+      double* d = q + (base - rs + k) * ld;
+      if (full_store)
+        *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+      else if (live) {
+        if (col >= c0 && col < c1) d[0] = o0;
+        if (col + 1 >= c0 && col + 1 < c1) d[1] = o1;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < 2; v++) {
+      w[0][v] = w[GROUP][v];
+      w[1][v] = w[GROUP + 1][v];
+    }
+  }
+}
+
 int main() {
   const long n = 8192;
   const size_t bytes = n * n * 8;
@@ -503,11 +571,15 @@ int main() {
     dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));      \
     march9f<ROWS, G, MINB><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);                         \
   })
-  M9F(16, 4, 5);
-  M9F(16, 4, 4);
-  M9F(32, 4, 5);
-  M9F(16, 2, 5);
-  M9F(16, 2, 6);
+#define M9Q(ROWS, G, MINB)                                                                     \
+  time_it("st9q R" #ROWS " G" #G " minB" #MINB, [&] {                                           \
+    dim3 g((unsigned)((c1 - cbase + 511) / 512), (unsigned)((r1 - r0 + ROWS - 1) / ROWS));      \
+    march9q<ROWS, G, MINB><<<g, 256>>>(X, Y, n, r0, r1, c0, c1, cbase);                         \
+  })
+  M9Q(16, 4, 5);
+  M9Q(16, 4, 4);
+  M9Q(32, 4, 5);
+  M9Q(16, 2, 6);
   // plain copy for reference bandwidth
   {
     cudaEventRecord(a);
