@@ -315,14 +315,16 @@ def test_config2_full_scale_eigenmode(H):
 
 
 # ------------------------------------------------------------------ multi-GPU
-@pytest.mark.skipif("ngpus() < 2")
-@pytest.mark.parametrize("P", [2, 4])
-def test_multi_gpu_single_process(H, P):
-    """P devices over 2 physical GPUs (NVLink peer pulls + cross-GPU sync words)."""
+@pytest.mark.parametrize("G,P", [(2, 2), (2, 4), (4, 8)])
+def test_multi_gpu_single_process(H, G, P):
+    """P devices over G physical GPUs (NVLink peer pulls + cross-GPU sync words; at P=8
+    the BLOCK grid is 4x2 and same-GPU and cross-GPU neighbours mix)."""
+    if ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
     shape = (258, 514)
     u0 = synth.uniform(3, shape)
     for transport in (0, 1, 2):
-        h = H.HDArray(n_gpus=2, n_devices=P)
+        h = H.HDArray(n_gpus=G, n_devices=P)
         h.set_transport(transport)
         w = O.Oracle(P)
         for be in (h, w):
@@ -336,6 +338,10 @@ def test_multi_gpu_single_process(H, P):
             for s in range(4):
                 src, dst = (X, Y) if s % 2 == 0 else (Y, X)
                 be.apply(H.K_STENCIL9, part, [(dst, [], [(0, 0)]), (src, N9, [])])
+            blk = be.partition(H.BLOCK, shape, (1, 1), (shape[0] - 1, shape[1] - 1))
+            for s in range(2):
+                src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+                be.apply(H.K_STENCIL9, blk, [(dst, [], [(0, 0)]), (src, N9, [])])
             be.apply(H.K_SCALE, colp, [(X, [(0, 0)], [(0, 0)])], [2.0])
         assert_replicas(h, w, [X, Y], P)
         h.close()
@@ -343,7 +349,7 @@ def test_multi_gpu_single_process(H, P):
     big = (1024, 2048)
     v = synth.uniform(8, big, "f32")
     for transport in (0, 2):
-        h = H.HDArray(n_gpus=2, n_devices=P)
+        h = H.HDArray(n_gpus=G, n_devices=P)
         h.set_transport(transport)
         w = O.Oracle(P)
         for be in (h, w):

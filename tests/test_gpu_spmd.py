@@ -128,20 +128,32 @@ def _worker(rank, world, port, q, env1):
 @pytest.mark.parametrize("env1", [{}, {"HDA_DEBUG_PULL_DELAY_US": "300"},
                                   {"HDA_DEBUG_PULL_DELAY_US": "300", "HDA_HALO_MODE": "1"}],
                          ids=["plain", "slow-reader", "slow-reader-fused"])
-def test_spmd_two_gpus(env1):
-    import torch
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
-    world = 2
+def _run(world, env1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     ps = [ctx.Process(target=_worker, args=(r, world, port, q, env1)) for r in range(world)]
     for p in ps:
         p.start()
-    out = [q.get(timeout=240) for _ in ps]
+    out = [q.get(timeout=300) for _ in ps]
     for p in ps:
         p.join(timeout=60)
     for rank, bad, msgs, hits in out:
         assert not bad, (rank, bad)
         assert msgs > 0 and hits > 0
+
+
+def test_spmd_two_gpus(env1):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, env1)
+
+
+def test_spmd_four_gpus():
+    """4 ranks: ROW halos with two neighbours, BLOCK 2x2 with corners, a 4-way
+    repartition all-to-all and reductions, every replica against the oracle."""
+    import torch
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, {})
