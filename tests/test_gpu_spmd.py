@@ -123,11 +123,6 @@ def _worker(rank, world, port, q, env1):
         q.put((rank, ["exception", traceback.format_exc()], 0, 0))
 
 
-# HDA_DEBUG_PULL_DELAY_US makes rank 1's pulls sleep after their RAW waits: a writer
-# that overwrote cells without waiting for rank 1's ACK would break parity.
-@pytest.mark.parametrize("env1", [{}, {"HDA_DEBUG_PULL_DELAY_US": "300"},
-                                  {"HDA_DEBUG_PULL_DELAY_US": "300", "HDA_HALO_MODE": "1"}],
-                         ids=["plain", "slow-reader", "slow-reader-fused"])
 def _run(world, env1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -143,6 +138,11 @@ def _run(world, env1):
         assert msgs > 0 and hits > 0
 
 
+# HDA_DEBUG_PULL_DELAY_US makes rank 1's pulls sleep after their RAW waits: a writer
+# that overwrote cells without waiting for rank 1's ACK would break parity.
+@pytest.mark.parametrize("env1", [{}, {"HDA_DEBUG_PULL_DELAY_US": "300"},
+                                  {"HDA_DEBUG_PULL_DELAY_US": "300", "HDA_HALO_MODE": "1"}],
+                         ids=["plain", "slow-reader", "slow-reader-fused"])
 def test_spmd_two_gpus(env1):
     import torch
     if torch.cuda.device_count() < 2:
