@@ -299,6 +299,21 @@ cudaError_t launch_signal_pdl(const SignalList& l, int relaxed, cudaStream_t s) 
   return launch_pdl(signal_pdl_kernel, dim3(1), dim3(kMaxDev), s, l, relaxed);
 }
 
+// HDA_TAIL_ROWS (default 4; 0 = off) / HDA_TAIL_WAVES (default 1): rows per tile and
+// waves of the short tiles that end a many-wave 2-D stencil launch
+static int env_or(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+static int tail_rows() {
+  static const int v = env_or("HDA_TAIL_ROWS", 4);
+  return v;
+}
+static int tail_waves() {
+  static const int v = env_or("HDA_TAIL_WAVES", 1);
+  return v;
+}
+
 constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
 constexpr int ST_ROWS = 16;      // rows per block
@@ -614,6 +629,36 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
       bx.rpb[k] = (rows + gyk - 1) / gyk;
       bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
       bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
+    }
+    // Tail split (many-wave single box): the last rows become short tiles, dispatched
+    // last, so the final partial wave drains in a fraction of a 16-row tile's time.
+    if (!one_wave && bx.n == 1 && tail_rows() > 0 && bx.c1[0] - bx.c0[0] > 64) {
+      static int occ = 0;
+      if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_kernel<T, KIND, ROWS>, ST_THREADS, 0);
+        if (occ <= 0) occ = ST_MINB;
+      }
+      const int64_t tr = tail_rows();
+      const int64_t slots = (int64_t)sm_count_dev() * occ;
+      int64_t trows = (tail_waves() * slots + bx.gx[0] - 1) / bx.gx[0] * tr;
+      const int64_t rows = bx.r1[0] - bx.r0[0];
+      trows = std::min<int64_t>(trows, rows / 4) / tr * tr;
+      if (trows > 0) {
+        bx.n = 2;
+        bx.r0[1] = bx.r1[0] - trows;
+        bx.r1[1] = bx.r1[0];
+        bx.r1[0] = bx.r0[1];
+        bx.c0[1] = bx.c0[0];
+        bx.c1[1] = bx.c1[0];
+        bx.cbase[1] = bx.cbase[0];
+        bx.gx[1] = bx.gx[0];
+        for (int k = 0; k < 2; k++) {
+          const int64_t rk = bx.r1[k] - bx.r0[k];
+          bx.rpb[k] = k ? tr : ST_ROWS;
+          bx.gy[k] = (int)((rk + bx.rpb[k] - 1) / bx.rpb[k]);
+          bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
+        }
+      }
     }
     // bx.n == 0: nothing to compute, but the sync words must still move (one block)
     const int64_t grid = bx.n ? bx.tstart[bx.n] : 1;
