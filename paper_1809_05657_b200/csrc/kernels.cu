@@ -793,8 +793,8 @@ constexpr int S3_ZCH = 32;  // planes per block
 template <typename T>
 __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n1,
                                                          int64_t n2, int64_t z0, int64_t z1, int64_t y0, int64_t y1,
-                                                         int64_t x0, int64_t x1, int64_t xbase,
-                                                         const __grid_constant__ KSync ks) {
+                                                         int64_t x0, int64_t x1, int64_t xbase, int64_t nbig,
+                                                         int64_t zt, const __grid_constant__ KSync ks) {
   pdl_enter();
   ks_pre(ks);
   constexpr int V = V16<T>::n;
@@ -802,7 +802,11 @@ __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ 
   const int64_t x = xbase + ((int64_t)blockIdx.x * 256 + threadIdx.x) * V;
   const int64_t ya = y0 + (int64_t)blockIdx.y * S3_R;
   const bool live = x < n2;
-  const int64_t zs = z0 + (int64_t)blockIdx.z * S3_ZCH, ze = min(zs + (int64_t)S3_ZCH, z1);
+  // chunks [0, nbig) hold S3_ZCH planes; the rest (dispatched last) zt planes each,
+  // so the final partial wave drains quickly
+  const int64_t bz = blockIdx.z;
+  const int64_t zs = bz < nbig ? z0 + bz * S3_ZCH : z0 + nbig * S3_ZCH + (bz - nbig) * zt;
+  const int64_t ze = min(zs + (bz < nbig ? (int64_t)S3_ZCH : zt), z1);
   const int64_t pl = n1 * n2;
   auto ld = [&](T(&r)[V], int64_t z, int64_t yy) {
     if (live && yy < n1) {
@@ -901,10 +905,27 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
   if (vec) {
     const int64_t xbase = lb[2] - (lb[2] % V);
     const int64_t per = 256 * V;
-    dim3 grid((unsigned)((ub[2] - xbase + per - 1) / per), (unsigned)((ub[1] - lb[1] + S3_R - 1) / S3_R),
-              (unsigned)((ub[0] - lb[0] + S3_ZCH - 1) / S3_ZCH));
+    const int64_t gx = (ub[2] - xbase + per - 1) / per, gy = (ub[1] - lb[1] + S3_R - 1) / S3_R;
+    const int64_t nz = ub[0] - lb[0];
+    int64_t nbig = (nz + S3_ZCH - 1) / S3_ZCH, zt = S3_ZCH, ntail = 0;
+    if (tail_rows() > 0 && nz > 4 * S3_ZCH) {
+      // about one wave of 4-plane chunks at the end (HDA_TAIL_ROWS = 0 turns it off)
+      static int occ = 0;
+      if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil7_kernel<T>, 256, 0);
+        if (occ <= 0) occ = 4;
+      }
+      zt = 4;
+      const int64_t slots = (int64_t)sm_count_dev() * occ;
+      int64_t tplanes = (slots + gx * gy - 1) / (gx * gy) * zt;
+      tplanes = std::min<int64_t>(tplanes, nz / 4);
+      nbig = (nz - tplanes) / S3_ZCH;
+      const int64_t rest = nz - nbig * S3_ZCH;
+      ntail = (rest + zt - 1) / zt;
+    }
+    dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)(nbig + ntail));
     cudaError_t e = launch_pdl(stencil7_kernel<T>, grid, dim3(256), s, in, out, n1, n2, lb[0], ub[0], lb[1], ub[1],
-                               lb[2], ub[2], xbase, ks);
+                               lb[2], ub[2], xbase, nbig, zt, ks);
     if (e != cudaSuccess) return e;
   } else {
     dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));
