@@ -304,6 +304,23 @@ class Repartition:
         self.prepared[self.calls % 2]()
         self.calls += 1
 
+    def e2e_setup(self, torch):
+        self.hX = torch.empty(self.shape, dtype=torch.float32).pin_memory()
+        self.hX.numpy()[:] = 1.0
+        self.hY = torch.empty(self.shape, dtype=torch.float32).pin_memory()
+        self.e2e_units = 2 * self.units  # two redistributions per job
+        lb, ub = self.h.region(self.rowp, self.rank, 2)
+        b = (ub[0] - lb[0]) * (ub[1] - lb[1]) * 4
+        self.e2e_bytes = (b, b)
+        self.e2e_desc = ("one job: hda_write X by rows -> SCALE by columns -> SCALE by rows -> hda_read X "
+                         "(host wall clock, pinned)")
+
+    def e2e_job(self):
+        self.h.write_ptr(self.X, self.rowp, self.hX.data_ptr())
+        self.prepared[0]()
+        self.prepared[1]()
+        self.h.read_ptr(self.X, self.rowp, self.hY.data_ptr())
+
     def reset_input(self):
         pass
 
@@ -358,6 +375,22 @@ class Gemm:
     def reset_input(self):
         pass
 
+    # end to end: pinned H2D of A and B, the product (incl. B's all-gather), D2H of C
+    def e2e_setup(self, torch):
+        self.hA = torch.from_numpy(self.Ab.view(np.int16)).pin_memory()
+        self.hB = torch.from_numpy(self.Bb.view(np.int16)).pin_memory()
+        self.hC = torch.empty((self.n, self.n), dtype=torch.float32).pin_memory()
+        self.e2e_units = 2.0 * self.n ** 3
+        rows = self.my_rows
+        self.e2e_bytes = (2 * rows * self.n * 2, rows * self.n * 4)
+        self.e2e_desc = "one job: hda_write A, B -> C = A @ B (B all-gathered) -> hda_read C (host wall clock, pinned)"
+
+    def e2e_job(self):
+        self.h.write_ptr(self.A, self.part, self.hA.data_ptr())
+        self.h.write_ptr(self.B, self.part, self.hB.data_ptr())
+        self.step()
+        self.h.read_ptr(self.C, self.part, self.hC.data_ptr())
+
     def parity(self):
         got = self.h.read(self.C, self.part)
         lb, ub = self.h.region(self.part, self.rank, 2)
@@ -410,6 +443,20 @@ class TwoMM:
 
     def reset_input(self):
         pass
+
+    def e2e_setup(self, torch):
+        self.hin = [torch.from_numpy(v.view(np.int16)).pin_memory() for v in (self.Ab, self.Bb, self.Cb)]
+        self.hE = torch.empty((self.n, self.n), dtype=torch.float32).pin_memory()
+        self.e2e_units = self.flops_per_step
+        cells = (self.ub[0] - self.lb[0]) * (self.ub[1] - self.lb[1])
+        self.e2e_bytes = (3 * cells * 2, cells * 4)
+        self.e2e_desc = "one job: hda_write A, B, C -> D = A @ B, E = C @ D -> hda_read E (host wall clock, pinned)"
+
+    def e2e_job(self):
+        for X, hx in zip((self.A, self.B, self.C), self.hin):
+            self.h.write_ptr(X, self.part, hx.data_ptr())
+        self.step()
+        self.h.read_ptr(self.E, self.part, self.hE.data_ptr())
 
     def parity(self):
         """D sampled against the exact integer product rounded to bf16 (RNE); E sampled
@@ -666,6 +713,22 @@ def main():
         e2e = {"value": wl.units * args.e2e_sweeps / e2e_s / 1e9, "unit": "GPoints/s",
                "h2d_bytes_per_step": int(reduce(my_bytes, SUM)), "d2h_bytes_per_step": int(reduce(my_bytes, SUM)),
                "step": f"one job: hda_write -> {args.e2e_sweeps} sweeps -> hda_read (host wall clock, pinned)"}
+
+    elif not args.no_e2e and hasattr(wl, "e2e_job"):
+        wl.e2e_setup(torch)
+        times = []
+        for j in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            wl.e2e_job()
+            barrier()
+            if j:
+                times.append(time.perf_counter() - t0)
+        e2e_s = reduce(min(times), MAX)
+        scale = 1e12 if wl.metric_unit == "TFLOP/s" else 1e9
+        e2e = {"value": wl.e2e_units / e2e_s / scale, "unit": wl.metric_unit,
+               "h2d_bytes_per_step": int(reduce(wl.e2e_bytes[0], SUM)),
+               "d2h_bytes_per_step": int(reduce(wl.e2e_bytes[1], SUM)), "step": wl.e2e_desc}
 
     launches = int(reduce(launches, SUM))
     if rank == 0:
