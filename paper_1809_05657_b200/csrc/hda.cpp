@@ -32,6 +32,11 @@
 #include <memory>
 #include <string>
 #include <unordered_map>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "hdarray.h"
@@ -125,6 +130,72 @@ struct ExecPlan {
 
 }  // namespace
 
+// One host thread per GPU for single-process contexts: a call's launches for the
+// devices of different GPUs are issued concurrently (each GPU's own order is kept;
+// across GPUs the device-side sync words order everything, as between SPMD ranks).
+// Measured serial issue: ~10 us per device per call, i.e. host-bound beyond ~4 GPUs.
+// Workers spin briefly between calls, then sleep on a condition variable.
+class IssuePool {
+ public:
+  explicit IssuePool(const std::vector<int>& ordinals) : ord_(ordinals), rcs_(ordinals.size(), 0) {
+    for (size_t g = 0; g < ord_.size(); g++) th_.emplace_back([this, g] { worker((int)g); });
+  }
+  ~IssuePool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_.store(true);
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // fn(gpu index) on every worker; returns the first nonzero result
+  int run(const std::function<int(int)>& fn) {
+    task_ = &fn;
+    remaining_.store((int)ord_.size(), std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    while (remaining_.load(std::memory_order_acquire) > 0) std::this_thread::yield();
+    for (int r : rcs_)
+      if (r) return r;
+    return 0;
+  }
+
+ private:
+  void worker(int g) {
+    cudaSetDevice(ord_[g]);
+    uint64_t seen = 0;
+    for (;;) {
+      int spins = 0;
+      uint64_t cur;
+      while ((cur = gen_.load(std::memory_order_acquire)) == seen && !stop_.load()) {
+        if (++spins < 4096) {
+          std::this_thread::yield();
+        } else {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return gen_.load() != seen || stop_.load(); });
+          spins = 0;
+        }
+      }
+      if (stop_.load()) return;
+      seen = cur;
+      rcs_[g] = (*task_)(g);
+      remaining_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  std::vector<int> ord_;
+  std::vector<int> rcs_;
+  std::vector<std::thread> th_;
+  const std::function<int(int)>* task_ = nullptr;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> remaining_{0};
+  std::atomic<bool> stop_{false};
+  std::mutex mu_;
+  std::condition_variable cv_;
+};
+
 struct hda_ctx {
   int P = 0;
   bool spmd = false, plan_only = false, sync_imported = true;
@@ -158,6 +229,8 @@ struct hda_ctx {
   int sticky = 0;
   std::string err;
   hda_stats_t stats{};
+  std::mutex err_mu;
+  std::unique_ptr<IssuePool> pool;  // single-process, >= 2 GPUs (issue_pool)
   std::vector<hda_msg_t> last_plan;
   long long timeout_ns = 60LL * 1000 * 1000 * 1000;
 };
@@ -165,11 +238,15 @@ struct hda_ctx {
 // ====================================================================== helpers
 
 static int fail(hda_ctx_t* c, int code, const std::string& m) {
-  if (c) c->err = m;
+  if (c) {
+    std::lock_guard<std::mutex> lk(c->err_mu);
+    c->err = m;
+  }
   return code;
 }
 
 static int cuda_fail(hda_ctx_t* c, cudaError_t e, const char* what) {
+  std::lock_guard<std::mutex> lk(c->err_mu);
   c->sticky = HDA_ECUDA;
   c->err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
   return HDA_ECUDA;
@@ -266,7 +343,18 @@ static void batch_descs(std::vector<RunDesc>& descs, std::vector<RunBatch>& out)
   if (b.n) out.push_back(b);
 }
 
-static void count_launch(hda_ctx_t* ctx, int n = 1) { ctx->stats.kernel_launches += n; }
+// devices' launches may be issued from several host threads (IssuePool)
+static void count_launch(hda_ctx_t* ctx, int n = 1) {
+  __atomic_fetch_add(&ctx->stats.kernel_launches, (int64_t)n, __ATOMIC_RELAXED);
+}
+// trace/timing attribution of the next timed_end (serial issue only: timing and tracing
+// turn the issue threads off)
+static void mark(hda_ctx_t* ctx, int q, int phase) {
+  if (ctx->ktiming || ctx->tracing) {
+    ctx->cur_dev = q;
+    ctx->cur_phase = phase;
+  }
+}
 
 static cudaEvent_t get_event(hda_ctx_t* ctx) {
   if (!ctx->ev_pool.empty()) {
@@ -570,11 +658,13 @@ static int timed_end(hda_ctx_t* ctx, cudaStream_t st, int kind, cudaEvent_t a, i
   return HDA_OK;
 }
 
-static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k, bool overlap_kernel,
-                       bool halo_kernel) {
+// exec plan of call t (cached per transition) and the WAR bookkeeping of its reads
+// (`scratch` holds the plan when the cache is off; it must outlive the issue)
+static int exchange_plan(hda_ctx_t* ctx, const Transition* t, unsigned long long k, ExecPlan& scratch,
+                         ExecPlan** out) {
+  *out = nullptr;
   if (t->msgs.empty()) return HDA_OK;
   ExecPlan* ep;
-  ExecPlan scratch;
   if (ctx->cache_on) {
     auto it = ctx->exec.find(t->serial);
     if (it == ctx->exec.end() || it->second.transport != ctx->transport) {
@@ -590,85 +680,89 @@ static int do_exchange(hda_ctx_t* ctx, const Transition* t, unsigned long long k
     if (rc) return rc;
     ep = &scratch;
   }
-  if (!ep->staged) {
+  if (!ep->staged)
     for (const PendEntry& e : ep->reads) ctx->pend[e.array][e.src][e.dst] = k;
-    for (PullJob& job : ep->pulls) {
-      const int q = job.dst;
-      CK(cudaSetDevice(ordinal_of(ctx, q)));
-      Gpu& g = ctx->gpus[ctx->dev[q].gpu];
-      // 2-D stencil with a cross-GPU halo: the pull runs inside the stencil launch
-      if (ctx->overlap && halo_kernel && job.cross && job.split && job.ce.empty() && job.batches.size() == 1 &&
-          job.srcs.size() <= 8 && job.interior.size() + job.dependent.size() <= 8) {
-        ctx->halo_job[q] = &job;
-        for (auto& pr : job.pend) ctx->pend[pr.first][pr.second][q] = k;
-        continue;
-      }
-      const bool comm = ctx->overlap && job.cross && job.split && overlap_kernel;
-      cudaStream_t st = comm ? g.comm : g.stream;
-      if (comm) {  // the pull may start as soon as everything issued before this call is done
-        CK(cudaEventRecord(g.ev_fork, g.stream));
-        CK(cudaStreamWaitEvent(g.comm, g.ev_fork, 0));
-        ctx->pulled_on_comm[q] = 1;
-        ctx->cur_pull[q] = &job;
-      }
-      // RAW waits and ACK signals ride in the pull kernel itself (sync.cuh)
-      KSync pre = ks_empty(ctx), post = ks_empty(ctx);
-      post.sig_val = k;
-      post.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
-      for (int p : job.srcs)
-        if (!same_stream(ctx, p, q)) {
-          ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
-          ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
-        }
-      int rc;
-      cudaEvent_t a = nullptr;
-      const size_t nb = job.batches.size();
-      if (job.ce.empty() && (rc = timed_begin(ctx, st, &a))) return rc;
-      if (!job.ce.empty()) {  // copy-engine part: RAW wait kernel, then the copies
-        KSync w = ks_empty(ctx);
-        std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
-        std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
-        w.nwait = pre.nwait;
-        w.delay_ns = pull_delay_ns();
-        RunBatch empty;
-        std::memset(&empty, 0, sizeof empty);
-        if (w.nwait || w.delay_ns) {
-          CK(launch_copy_runs(empty, w, st));
-          count_launch(ctx);
-        }
-        pre.nwait = 0;
-        if ((rc = timed_begin(ctx, st, &a))) return rc;  // transfer time, not the wait
-        for (const cudaMemcpy3DParms& p : job.ce) CK(cudaMemcpy3DAsync(&p, st));
-        if (nb == 0) {
-          CK(launch_copy_runs(empty, post, st));  // ACK signals after the copies
-          count_launch(ctx);
-        }
-      }
-      for (size_t i = 0; i < nb; i++) {
-        KSync ks = ks_empty(ctx);
-        if (i == 0) {
-          std::memcpy(ks.wait_ptr, pre.wait_ptr, sizeof ks.wait_ptr);
-          std::memcpy(ks.wait_val, pre.wait_val, sizeof ks.wait_val);
-          ks.nwait = pre.nwait;
-          ks.delay_ns = pull_delay_ns();
-        }
-        if (i + 1 == nb) {
-          std::memcpy(ks.sig_ptr, post.sig_ptr, sizeof ks.sig_ptr);
-          ks.nsig = post.nsig;
-          ks.sig_val = post.sig_val;
-          ks.ctr = post.ctr;
-        }
-        CK(launch_copy_runs(job.batches[i], ks, st));
-        count_launch(ctx);
-      }
-      ctx->cur_dev = q;
-      if ((rc = timed_end(ctx, st, -100, a))) return rc;
-      if (comm) CK(cudaEventRecord(g.ev_pull, g.comm));
-      for (auto& pr : job.pend) ctx->pend[pr.first][pr.second][q] = k;
-    }
+  *out = ep;
+  return HDA_OK;
+}
+
+// one device's pull (reader q = job.dst): thread-safe against the other devices' issue
+static int issue_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k, bool overlap_kernel, bool halo_kernel) {
+  const int q = job.dst;
+  CK(cudaSetDevice(ordinal_of(ctx, q)));
+  Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+  // 2-D stencil with a cross-GPU halo: the pull runs inside the stencil launch
+  if (ctx->overlap && halo_kernel && job.cross && job.split && job.ce.empty() && job.batches.size() == 1 &&
+      job.srcs.size() <= 8 && job.interior.size() + job.dependent.size() <= 8) {
+    ctx->halo_job[q] = &job;
     return HDA_OK;
   }
-  // STAGED
+  const bool comm = ctx->overlap && job.cross && job.split && overlap_kernel;
+  cudaStream_t st = comm ? g.comm : g.stream;
+  if (comm) {  // the pull may start as soon as everything issued before this call is done
+    CK(cudaEventRecord(g.ev_fork, g.stream));
+    CK(cudaStreamWaitEvent(g.comm, g.ev_fork, 0));
+    ctx->pulled_on_comm[q] = 1;
+    ctx->cur_pull[q] = &job;
+  }
+  // RAW waits and ACK signals ride in the pull kernel itself (sync.cuh)
+  KSync pre = ks_empty(ctx), post = ks_empty(ctx);
+  post.sig_val = k;
+  post.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
+  for (int p : job.srcs)
+    if (!same_stream(ctx, p, q)) {
+      ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
+      ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
+    }
+  int rc;
+  cudaEvent_t a = nullptr;
+  const size_t nb = job.batches.size();
+  if (job.ce.empty() && (rc = timed_begin(ctx, st, &a))) return rc;
+  if (!job.ce.empty()) {  // copy-engine part: RAW wait kernel, then the copies
+    KSync w = ks_empty(ctx);
+    std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
+    std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
+    w.nwait = pre.nwait;
+    w.delay_ns = pull_delay_ns();
+    RunBatch empty;
+    std::memset(&empty, 0, sizeof empty);
+    if (w.nwait || w.delay_ns) {
+      CK(launch_copy_runs(empty, w, st));
+      count_launch(ctx);
+    }
+    pre.nwait = 0;
+    if ((rc = timed_begin(ctx, st, &a))) return rc;  // transfer time, not the wait
+    for (const cudaMemcpy3DParms& p : job.ce) CK(cudaMemcpy3DAsync(&p, st));
+    if (nb == 0) {
+      CK(launch_copy_runs(empty, post, st));  // ACK signals after the copies
+      count_launch(ctx);
+    }
+  }
+  for (size_t i = 0; i < nb; i++) {
+    KSync ks = ks_empty(ctx);
+    if (i == 0) {
+      std::memcpy(ks.wait_ptr, pre.wait_ptr, sizeof ks.wait_ptr);
+      std::memcpy(ks.wait_val, pre.wait_val, sizeof ks.wait_val);
+      ks.nwait = pre.nwait;
+      ks.delay_ns = pull_delay_ns();
+    }
+    if (i + 1 == nb) {
+      std::memcpy(ks.sig_ptr, post.sig_ptr, sizeof ks.sig_ptr);
+      ks.nsig = post.nsig;
+      ks.sig_val = post.sig_val;
+      ks.ctr = post.ctr;
+    }
+    CK(launch_copy_runs(job.batches[i], ks, st));
+    count_launch(ctx);
+  }
+  mark(ctx, q, 0);
+  if ((rc = timed_end(ctx, st, -100, a))) return rc;
+  if (comm) CK(cudaEventRecord(g.ev_pull, g.comm));
+  return HDA_OK;
+}
+
+// STAGED transport (single process, serial issue)
+static int issue_staged(hda_ctx_t* ctx, ExecPlan* ep, unsigned long long k) {
   for (PackJob& job : ep->packs) {
     const int p = job.src;
     CK(cudaSetDevice(ordinal_of(ctx, p)));
@@ -924,6 +1018,188 @@ static bool arrays_ready(hda_ctx_t* ctx, const CallInfo& ci) {
 using clk = std::chrono::steady_clock;
 
 // the full per-call pipeline shared by apply / read / write
+// the issue threads, when they apply: single process, >= 2 local GPUs, no kernel
+// timing or tracing (their event bookkeeping is serial).  HDA_ISSUE_THREADS=0 disables.
+static IssuePool* issue_pool(hda_ctx_t* ctx) {
+  static const int on = env_int("HDA_ISSUE_THREADS", 1);
+  if (!on || ctx->spmd || ctx->plan_only || ctx->gpus.size() < 2 || ctx->ktiming || ctx->tracing) return nullptr;
+  if (!ctx->pool) {
+    std::vector<int> ord;
+    for (const Gpu& g : ctx->gpus) ord.push_back(g.ordinal);
+    ctx->pool = std::make_unique<IssuePool>(ord);
+  }
+  return ctx->pool.get();
+}
+
+// everything device q issues for call k after its pull: WAR waits, the kernel (or the
+// host copy of a write/read), PROD signals.  Thread-safe against other devices' issue.
+static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long k, int q, int32_t kernel,
+                        const double* scalars, const void* host_in, void* host_out) {
+  const CallInfo& ci = *t->info;
+  const TPart& pt = ctx->tr->part(ci.part);
+  int rc;
+  bool defines = false;
+  for (size_t i = 0; i < ci.arrays.size(); i++)
+    if (!ci.ldef[i][q].empty()) defines = true;
+  const bool has_work = !box_empty(pt.box[q]);
+  const bool kern = kernel > KN_NONE && (kernel == KN_STAMP ? defines : has_work);
+  const bool io = (kernel == KN_WRITE && has_work) || (kernel == KN_READ && has_work);
+  if (!defines && !kern && !io) return HDA_OK;
+  CK(cudaSetDevice(ordinal_of(ctx, q)));
+  KSync ks = ks_empty(ctx);
+  if (defines) {
+    war_waits(ctx, ci, q, ks);
+    signal_prod(ctx, q, k, ks);
+    // HDA_DEBUG_FAKE_SIGNAL=1: a kernel with no peer to signal still runs the
+    // end-of-kernel fence + counter + store (to a local word) — measures their cost
+    static const int fake_sig = env_int("HDA_DEBUG_FAKE_SIGNAL", 0);
+    if (fake_sig && ks.nsig == 0) ks_sig(ks, ctx->dev[q].sync + SW_DEBUG);
+  }
+  // user kernels publish PROD from a trailing signal launch (HDA_SIG_KERNEL=0: from
+  // the kernel's last CTA, after a fence in every CTA)
+  static const int sig_kernel = env_int("HDA_SIG_KERNEL", 1);
+  SignalList post_sig;
+  post_sig.n = 0;
+  const bool split_sig = sig_kernel && kern && !io && ks.nsig > 0;
+  if (split_sig) {
+    for (int i = 0; i < ks.nsig; i++) post_sig.ptr[i] = ks.sig_ptr[i];
+    post_sig.n = ks.nsig;
+    post_sig.val = ks.sig_val;
+    ks.nsig = 0;
+  }
+  const int X0 = ci.param_array[0];
+  const TArray& a0 = ctx->tr->array(X0);
+  if (io) {
+    // host copies cannot carry sync words: separate wait before, signal after
+    KSync pre = ks_empty(ctx), post = ks_empty(ctx);
+    std::memcpy(pre.wait_ptr, ks.wait_ptr, sizeof pre.wait_ptr);
+    std::memcpy(pre.wait_val, ks.wait_val, sizeof pre.wait_val);
+    pre.nwait = ks.nwait;
+    std::memcpy(post.sig_ptr, ks.sig_ptr, sizeof post.sig_ptr);
+    post.nsig = ks.nsig;
+    post.sig_val = ks.sig_val;
+    post.ctr = ks.ctr;
+    if ((rc = sync_only(ctx, q, pre))) return rc;
+    int64_t S[3];
+    front_shape(a0.ndim, a0.shape, S);
+    Box fb = front_box(a0.ndim, pt.box[q]);
+    cudaMemcpy3DParms p;
+    std::memset(&p, 0, sizeof p);
+    const size_t es = a0.es;
+    void* host = kernel == KN_WRITE ? const_cast<void*>(host_in) : host_out;
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)S[2] * es, (size_t)S[2], (size_t)S[1]);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(ctx->arr[X0].ptr[q], (size_t)S[2] * es, (size_t)S[2], (size_t)S[1]);
+    cudaPos pos = make_cudaPos((size_t)fb.lb[2] * es, (size_t)fb.lb[1], (size_t)fb.lb[0]);
+    p.extent = make_cudaExtent((size_t)(fb.ub[2] - fb.lb[2]) * es, (size_t)(fb.ub[1] - fb.lb[1]),
+                               (size_t)(fb.ub[0] - fb.lb[0]));
+    if (kernel == KN_WRITE) {
+      p.srcPtr = hp;
+      p.srcPos = pos;
+      p.dstPtr = dp;
+      p.dstPos = pos;
+      p.kind = cudaMemcpyHostToDevice;
+    } else {
+      p.srcPtr = dp;
+      p.srcPos = pos;
+      p.dstPtr = hp;
+      p.dstPos = pos;
+      p.kind = cudaMemcpyDeviceToHost;
+    }
+    if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
+    if ((rc = sync_only(ctx, q, post))) return rc;
+  } else if (kern && ctx->halo_job[q]) {
+    // fused halo-exchange stencil: pull + interior + dependent strips, one launch
+    const PullJob& job = *ctx->halo_job[q];
+    ctx->halo_job[q] = nullptr;
+    const CallInfo& ci = *t->info;
+    const TArray& a0 = ctx->tr->array(ci.param_array[0]);
+    int64_t S[3];
+    front_shape(a0.ndim, a0.shape, S);
+    std::vector<Box> fb;
+    for (const Box& b : job.interior) fb.push_back(front_box(a0.ndim, b));
+    for (const Box& b : job.dependent) fb.push_back(front_box(a0.ndim, b));
+    const int64_t* lbs[8];
+    const int64_t* ubs[8];
+    for (size_t i = 0; i < fb.size(); i++) {
+      lbs[i] = fb[i].lb;
+      ubs[i] = fb[i].ub;
+    }
+    HaloPull hp;
+    std::memset(&hp, 0, sizeof hp);
+    for (int p : job.srcs)
+      if (!same_stream(ctx, p, q)) {
+        if (ctx->last_prod[p]) {
+          hp.wait_ptr[hp.nwait] = ctx->dev[q].sync + SW_PROD + p;
+          hp.wait_val[hp.nwait++] = ctx->last_prod[p];
+        }
+        hp.ack_ptr[hp.nack++] = ctx->dev[p].sync + SW_ACK + q;
+      }
+    hp.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
+    hp.done_word = ctx->dev[q].sync + SW_PULLDONE;
+    hp.epoch = k;
+    hp.delay_ns = pull_delay_ns();
+    auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
+    cudaStream_t st = stream_of(ctx, q);
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, st, &a))) return rc;
+    CK(launch_stencil2d_halo(kernel, a0.dtype, P_(1), P_(0), S, lbs, ubs, (int)fb.size(),
+                             (int)job.interior.size(), job.batches[0], hp, ks, st));
+    count_launch(ctx);
+    mark(ctx, q, 1);
+    if ((rc = timed_end(ctx, st, kernel, a, 1))) return rc;
+  } else if (kern && ctx->pulled_on_comm[q]) {
+    // interior boxes while the pull is in flight, dependent boxes after it
+    const PullJob& job = *ctx->cur_pull[q];
+    Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+    bool joined = false;
+    const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
+    if (ks.nwait > 0) {
+      // The peers' pulls this WAR wait depends on need SM time (their pull kernels)
+      // or stall behind GPU-filling kernels (measured: cross-process 3-D peer copies
+      // on the copy engine); if every CTA of the interior spun here while the peers
+      // did the same, neither GPU would free what the other's pull needs.  Wait in
+      // one CTA, then launch the interior with no waits.
+      KSync w = ks_empty(ctx);
+      std::memcpy(w.wait_ptr, ks.wait_ptr, sizeof w.wait_ptr);
+      std::memcpy(w.wait_val, ks.wait_val, sizeof w.wait_val);
+      w.nwait = ks.nwait;
+      if ((rc = sync_only(ctx, q, w))) return rc;
+      ks.nwait = 0;
+    }
+    if (has_i) {
+      cudaEvent_t a;
+      if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+      if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, true, !has_d), &job.interior))) return rc;
+      mark(ctx, q, 2);
+      if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
+    }
+    if (has_d) {
+      CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+      joined = true;
+      cudaEvent_t a;
+      if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+      if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, !has_i, true), &job.dependent))) return rc;
+      mark(ctx, q, 3);
+      if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
+    }
+    if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+    ctx->pulled_on_comm[q] = 0;
+  } else if (kern) {
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, stream_of(ctx, q), &a))) return rc;
+    if ((rc = run_kernel(ctx, t, q, scalars, ks))) return rc;
+    mark(ctx, q, 1);
+    if ((rc = timed_end(ctx, stream_of(ctx, q), kernel, a))) return rc;
+  } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
+    return rc;
+  }
+  if (split_sig) {
+    CK(launch_signal_pdl(post_sig, ks.relaxed, stream_of(ctx, q)));
+    count_launch(ctx);
+  }
+  return HDA_OK;
+}
+
 static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn* acc, int32_t n_acc,
                 const double* scalars, int32_t n_scalars, const void* host_in, void* host_out) {
   auto t0 = clk::now();
@@ -947,173 +1223,32 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     static const int halo_mode = env_int("HDA_HALO_MODE", -1);
     const bool halo_kernel = (halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9)) ||
                              (halo_mode == -1 && kernel == KN_JACOBI5);
-    if ((rc = do_exchange(ctx, t, k, overlap_kernel, halo_kernel))) return rc;
-    const TPart& pt = ctx->tr->part(part);
-    for (int q = 0; q < ctx->P; q++) {
-      if (!ctx->dev[q].local) continue;
-      bool defines = false;
-      for (size_t i = 0; i < ci.arrays.size(); i++)
-        if (!ci.ldef[i][q].empty()) defines = true;
-      const bool has_work = !box_empty(pt.box[q]);
-      const bool kern = kernel > KN_NONE && (kernel == KN_STAMP ? defines : has_work);
-      const bool io = (kernel == KN_WRITE && has_work) || (kernel == KN_READ && has_work);
-      if (!defines && !kern && !io) continue;
-      CK(cudaSetDevice(ordinal_of(ctx, q)));
-      KSync ks = ks_empty(ctx);
-      if (defines) {
-        war_waits(ctx, ci, q, ks);
-        signal_prod(ctx, q, k, ks);
-        // HDA_DEBUG_FAKE_SIGNAL=1: a kernel with no peer to signal still runs the
-        // end-of-kernel fence + counter + store (to a local word) — measures their cost
-        static const int fake_sig = env_int("HDA_DEBUG_FAKE_SIGNAL", 0);
-        if (fake_sig && ks.nsig == 0) ks_sig(ks, ctx->dev[q].sync + SW_DEBUG);
-      }
-      // user kernels publish PROD from a trailing signal launch (HDA_SIG_KERNEL=0: from
-      // the kernel's last CTA, after a fence in every CTA)
-      static const int sig_kernel = env_int("HDA_SIG_KERNEL", 1);
-      SignalList post_sig;
-      post_sig.n = 0;
-      const bool split_sig = sig_kernel && kern && !io && ks.nsig > 0;
-      if (split_sig) {
-        for (int i = 0; i < ks.nsig; i++) post_sig.ptr[i] = ks.sig_ptr[i];
-        post_sig.n = ks.nsig;
-        post_sig.val = ks.sig_val;
-        ks.nsig = 0;
-      }
-      const int X0 = ci.param_array[0];
-      const TArray& a0 = ctx->tr->array(X0);
-      if (io) {
-        // host copies cannot carry sync words: separate wait before, signal after
-        KSync pre = ks_empty(ctx), post = ks_empty(ctx);
-        std::memcpy(pre.wait_ptr, ks.wait_ptr, sizeof pre.wait_ptr);
-        std::memcpy(pre.wait_val, ks.wait_val, sizeof pre.wait_val);
-        pre.nwait = ks.nwait;
-        std::memcpy(post.sig_ptr, ks.sig_ptr, sizeof post.sig_ptr);
-        post.nsig = ks.nsig;
-        post.sig_val = ks.sig_val;
-        post.ctr = ks.ctr;
-        if ((rc = sync_only(ctx, q, pre))) return rc;
-        int64_t S[3];
-        front_shape(a0.ndim, a0.shape, S);
-        Box fb = front_box(a0.ndim, pt.box[q]);
-        cudaMemcpy3DParms p;
-        std::memset(&p, 0, sizeof p);
-        const size_t es = a0.es;
-        void* host = kernel == KN_WRITE ? const_cast<void*>(host_in) : host_out;
-        cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)S[2] * es, (size_t)S[2], (size_t)S[1]);
-        cudaPitchedPtr dp = make_cudaPitchedPtr(ctx->arr[X0].ptr[q], (size_t)S[2] * es, (size_t)S[2], (size_t)S[1]);
-        cudaPos pos = make_cudaPos((size_t)fb.lb[2] * es, (size_t)fb.lb[1], (size_t)fb.lb[0]);
-        p.extent = make_cudaExtent((size_t)(fb.ub[2] - fb.lb[2]) * es, (size_t)(fb.ub[1] - fb.lb[1]),
-                                   (size_t)(fb.ub[0] - fb.lb[0]));
-        if (kernel == KN_WRITE) {
-          p.srcPtr = hp;
-          p.srcPos = pos;
-          p.dstPtr = dp;
-          p.dstPos = pos;
-          p.kind = cudaMemcpyHostToDevice;
-        } else {
-          p.srcPtr = dp;
-          p.srcPos = pos;
-          p.dstPtr = hp;
-          p.dstPos = pos;
-          p.kind = cudaMemcpyDeviceToHost;
-        }
-        if (host) CK(cudaMemcpy3DAsync(&p, stream_of(ctx, q)));
-        if ((rc = sync_only(ctx, q, post))) return rc;
-      } else if (kern && ctx->halo_job[q]) {
-        // fused halo-exchange stencil: pull + interior + dependent strips, one launch
-        const PullJob& job = *ctx->halo_job[q];
-        ctx->halo_job[q] = nullptr;
-        const CallInfo& ci = *t->info;
-        const TArray& a0 = ctx->tr->array(ci.param_array[0]);
-        int64_t S[3];
-        front_shape(a0.ndim, a0.shape, S);
-        std::vector<Box> fb;
-        for (const Box& b : job.interior) fb.push_back(front_box(a0.ndim, b));
-        for (const Box& b : job.dependent) fb.push_back(front_box(a0.ndim, b));
-        const int64_t* lbs[8];
-        const int64_t* ubs[8];
-        for (size_t i = 0; i < fb.size(); i++) {
-          lbs[i] = fb[i].lb;
-          ubs[i] = fb[i].ub;
-        }
-        HaloPull hp;
-        std::memset(&hp, 0, sizeof hp);
-        for (int p : job.srcs)
-          if (!same_stream(ctx, p, q)) {
-            if (ctx->last_prod[p]) {
-              hp.wait_ptr[hp.nwait] = ctx->dev[q].sync + SW_PROD + p;
-              hp.wait_val[hp.nwait++] = ctx->last_prod[p];
-            }
-            hp.ack_ptr[hp.nack++] = ctx->dev[p].sync + SW_ACK + q;
-          }
-        hp.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
-        hp.done_word = ctx->dev[q].sync + SW_PULLDONE;
-        hp.epoch = k;
-        hp.delay_ns = pull_delay_ns();
-        auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
-        cudaStream_t st = stream_of(ctx, q);
-        cudaEvent_t a;
-        if ((rc = timed_begin(ctx, st, &a))) return rc;
-        CK(launch_stencil2d_halo(kernel, a0.dtype, P_(1), P_(0), S, lbs, ubs, (int)fb.size(),
-                                 (int)job.interior.size(), job.batches[0], hp, ks, st));
-        count_launch(ctx);
-        ctx->cur_dev = q;
-        ctx->cur_phase = 1;
-        if ((rc = timed_end(ctx, st, kernel, a, 1))) return rc;
-      } else if (kern && ctx->pulled_on_comm[q]) {
-        // interior boxes while the pull is in flight, dependent boxes after it
-        const PullJob& job = *ctx->cur_pull[q];
-        Gpu& g = ctx->gpus[ctx->dev[q].gpu];
-        bool joined = false;
-        const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
-        if (ks.nwait > 0) {
-          // The peers' pulls this WAR wait depends on need SM time (their pull kernels)
-          // or stall behind GPU-filling kernels (measured: cross-process 3-D peer copies
-          // on the copy engine); if every CTA of the interior spun here while the peers
-          // did the same, neither GPU would free what the other's pull needs.  Wait in
-          // one CTA, then launch the interior with no waits.
-          KSync w = ks_empty(ctx);
-          std::memcpy(w.wait_ptr, ks.wait_ptr, sizeof w.wait_ptr);
-          std::memcpy(w.wait_val, ks.wait_val, sizeof w.wait_val);
-          w.nwait = ks.nwait;
-          if ((rc = sync_only(ctx, q, w))) return rc;
-          ks.nwait = 0;
-        }
-        if (has_i) {
-          cudaEvent_t a;
-          if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-          if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, true, !has_d), &job.interior))) return rc;
-          ctx->cur_dev = q;
-          ctx->cur_phase = 2;
-          if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
-        }
-        if (has_d) {
-          CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
-          joined = true;
-          cudaEvent_t a;
-          if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-          if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, !has_i, true), &job.dependent))) return rc;
-          ctx->cur_dev = q;
-          ctx->cur_phase = 3;
-          if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
-        }
-        if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
-        ctx->pulled_on_comm[q] = 0;
-      } else if (kern) {
-        cudaEvent_t a;
-        if ((rc = timed_begin(ctx, stream_of(ctx, q), &a))) return rc;
-        if ((rc = run_kernel(ctx, t, q, scalars, ks))) return rc;
-        ctx->cur_dev = q;
-        ctx->cur_phase = 1;
-        if ((rc = timed_end(ctx, stream_of(ctx, q), kernel, a))) return rc;
-      } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
-        return rc;
-      }
-      if (split_sig) {
-        CK(launch_signal_pdl(post_sig, ks.relaxed, stream_of(ctx, q)));
-        count_launch(ctx);
-      }
+    ExecPlan scratch;
+    ExecPlan* ep = nullptr;
+    if ((rc = exchange_plan(ctx, t, k, scratch, &ep))) return rc;
+    if (ep && ep->staged && (rc = issue_staged(ctx, ep, k))) return rc;
+    IssuePool* pool = issue_pool(ctx);
+    if (pool) {
+      // one host thread per GPU: its devices' pulls, then their kernels (stream order
+      // within a GPU as in the serial path; across GPUs the sync words order everything)
+      rc = pool->run([&](int gi) -> int {
+        int r;
+        if (ep && !ep->staged)
+          for (PullJob& job : ep->pulls)
+            if (ctx->dev[job.dst].gpu == gi && (r = issue_pull(ctx, job, k, overlap_kernel, halo_kernel))) return r;
+        for (int q = 0; q < ctx->P; q++)
+          if (ctx->dev[q].local && ctx->dev[q].gpu == gi &&
+              (r = issue_kernel(ctx, t, k, q, kernel, scalars, host_in, host_out)))
+            return r;
+        return HDA_OK;
+      });
+      if (rc) return rc;
+    } else {
+      if (ep && !ep->staged)
+        for (PullJob& job : ep->pulls)
+          if ((rc = issue_pull(ctx, job, k, overlap_kernel, halo_kernel))) return rc;
+      for (int q = 0; q < ctx->P; q++)
+        if (ctx->dev[q].local && (rc = issue_kernel(ctx, t, k, q, kernel, scalars, host_in, host_out))) return rc;
     }
   }
   for (int q = 0; q < ctx->P && !ctx->plan_only; q++)
@@ -1258,6 +1393,7 @@ int hda_init_spmd(hda_ctx_t** out, int32_t n_devices, int32_t rank, int32_t gpu_
 
 int hda_finalize(hda_ctx_t* ctx) {
   if (!ctx) return HDA_EINVAL;
+  ctx->pool.reset();  // join the issue threads before their streams go away
   if (!ctx->plan_only) {
     DevGuard g(true);
     for (auto& gp : ctx->gpus) {

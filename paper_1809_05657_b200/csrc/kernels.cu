@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <cstdlib>
 #include <utility>
@@ -235,15 +236,17 @@ struct V16<float> {
 // (128 threads x 32 rows x 8-row groups at 113 registers reached only 4.99 TB/s:
 // too few warps in flight).
 static int sm_count_dev() {
-  static int n[64] = {0};
+  static std::atomic<int> n[64];  // launches may come from several host threads
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (!n[dev]) {
-    cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
-    if (n[dev] <= 0) n[dev] = 148;
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    n[dev].store(v, std::memory_order_relaxed);
   }
-  return n[dev];
+  return v;
 }
 
 // HDA_ONE_WAVE=0 disables the one-wave row-range layout (A/B measurements)
@@ -635,11 +638,11 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     // (5-point only: 8192^2 Jacobi 390.7 -> 396.3 GPoints/s; the 9-point, 44 waves of
     // 5 CTAs/SM, gains nothing)
     if (KIND == 0 && !one_wave && bx.n == 1 && tail_rows() > 0 && bx.c1[0] - bx.c0[0] > 64) {
-      static int occ = 0;
-      if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_kernel<T, KIND, ROWS>, ST_THREADS, 0);
-        if (occ <= 0) occ = ST_MINB;
-      }
+      static const int occ = [] {  // thread-safe one-time init
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil2d_kernel<T, KIND, ROWS>, ST_THREADS, 0);
+        return o > 0 ? o : ST_MINB;
+      }();
       const int64_t tr = tail_rows();
       const int64_t slots = (int64_t)sm_count_dev() * occ;
       int64_t trows = (tail_waves() * slots + bx.gx[0] - 1) / bx.gx[0] * tr;
@@ -711,11 +714,11 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
   // of row-range blocks sized to the slots the pull blocks leave free (blocks that
   // miss the first wave would double the step); the boundary strips keep 16-row tiles
   // and run in the slots the pull blocks vacate.
-  static int occ = 0;
-  if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil2d_halo_kernel<T, KIND, ROWS>, ST_THREADS, 0);
-    if (occ <= 0) occ = 1;
-  }
+  static const int occ = [] {  // thread-safe one-time init
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil2d_halo_kernel<T, KIND, ROWS>, ST_THREADS, 0);
+    return o > 0 ? o : 1;
+  }();
   const int64_t wave = (int64_t)sm_count_dev() * occ;
   int64_t tiles16 = 0, strips_i = 0;
   for (int k = 0; k < bx.n; k++) {
@@ -910,11 +913,11 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
     int64_t nbig = (nz + S3_ZCH - 1) / S3_ZCH, zt = S3_ZCH, ntail = 0;
     if (tail_rows() > 0 && nz > 4 * S3_ZCH) {
       // about one wave of 4-plane chunks at the end (HDA_TAIL_ROWS = 0 turns it off)
-      static int occ = 0;
-      if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil7_kernel<T>, 256, 0);
-        if (occ <= 0) occ = 4;
-      }
+      static const int occ = [] {  // thread-safe one-time init
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, stencil7_kernel<T>, 256, 0);
+        return o > 0 ? o : 4;
+      }();
       zt = 4;
       const int64_t slots = (int64_t)sm_count_dev() * occ;
       int64_t tplanes = (slots + gx * gy - 1) / (gx * gy) * zt;
