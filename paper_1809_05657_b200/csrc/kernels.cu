@@ -726,6 +726,35 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     if (k < ni && bx.c1[k] - bx.c0[k] > 64) strips_i += bx.gx[k];
   }
   const bool one_wave = one_wave_enabled() && tiles16 < 5 * wave && strips_i > 0 && wave - npull >= strips_i;
+  // many-wave share (N=2) with one interior box: its last rows as a tail box of short
+  // tiles, dispatched after the interior and before the boundary strips (5-point only,
+  // as in the plain launch)
+  int tail_k = -1;
+  if (KIND == 0 && !one_wave && ni == 1 && bx.n < 8 && tail_rows() > 0 && bx.c1[0] - bx.c0[0] > 64) {
+    const int64_t tr = tail_rows();
+    int64_t trows = (tail_waves() * wave + bx.gx[0] - 1) / bx.gx[0] * tr;
+    trows = std::min<int64_t>(trows, (bx.r1[0] - bx.r0[0]) / 4) / tr * tr;
+    if (trows > 0) {
+      for (int k = bx.n; k > 1; k--) {  // shift the boundary boxes up by one
+        bx.r0[k] = bx.r0[k - 1];
+        bx.r1[k] = bx.r1[k - 1];
+        bx.c0[k] = bx.c0[k - 1];
+        bx.c1[k] = bx.c1[k - 1];
+        bx.cbase[k] = bx.cbase[k - 1];
+        bx.gx[k] = bx.gx[k - 1];
+      }
+      bx.n++;
+      bx.r0[1] = bx.r1[0] - trows;
+      bx.r1[1] = bx.r1[0];
+      bx.r1[0] = bx.r0[1];
+      bx.c0[1] = bx.c0[0];
+      bx.c1[1] = bx.c1[0];
+      bx.cbase[1] = bx.cbase[0];
+      bx.gx[1] = bx.gx[0];
+      ni = 2;
+      tail_k = 1;
+    }
+  }
   bx.tstart[0] = 0;
   for (int k = 0; k < bx.n; k++) {
     const int64_t rows = bx.r1[k] - bx.r0[k];
@@ -734,6 +763,7 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
       gyk = std::max<int64_t>(1, (wave - npull) / strips_i);
       gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
     }
+    if (k == tail_k) gyk = (rows + tail_rows() - 1) / tail_rows();  // short tiles
     bx.rpb[k] = (rows + gyk - 1) / gyk;
     bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
     bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
