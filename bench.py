@@ -743,6 +743,8 @@ def main():
                        "transport": ["fused", "staged", "auto"][args.transport], "overlap": not args.no_overlap,
                        "l2": ("L2 flushed between timed steps (write a 2x-L2 buffer, then read another)" if flush else
                               f"inputs larger than L2 (per-GPU working set {wl.working_set / 2**20:.0f} MiB)")},
+            **({"note": "one device: a repartition moves nothing (value 0); the roofline is the SCALE kernel's"}
+               if args.workload == "repartition" and ws == 1 else {}),
             "roofline": roof,
             "exchange": {"bytes_per_step": halo_bytes, "exchange_ms_per_step": x_avg if x_n else 0.0,
                          "GBps_per_gpu": (halo_bytes / ws / (x_avg * 1e-3) / 1e9) if x_n else None,
