@@ -166,7 +166,10 @@ typedef struct {
 /* ---- lifetime (Table 2 Init/Exit) ----
  * hda_init: gpu_ids[n_gpus] (NULL => 0..n_gpus-1); n_devices = P >= n_gpus
  * (device d runs on gpu_ids[d % n_gpus]); n_gpus == 0 => plan-only.
- * Enables peer access between all listed GPUs.  EINVAL if P < 1, P > 64. */
+ * Enables peer access between all listed GPUs.  EINVAL if P < 1, P > 64.
+ * A context is used from one host thread at a time (calls are not re-entrant); with
+ * >= 2 GPUs the context itself issues each GPU's launches from an internal per-GPU
+ * thread (joined before every call returns; HDA_ISSUE_THREADS=0 disables). */
 int hda_init(hda_ctx_t** out, int32_t n_gpus, const int32_t* gpu_ids, int32_t n_devices);
 /* hda_init_spmd: this process is device `rank` of n_devices, on CUDA device gpu_id
  * (gpu_id < 0 => plan-only SPMD context: tracker only, used for host-logic tests). */
