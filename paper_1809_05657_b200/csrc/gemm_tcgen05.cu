@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -27,6 +28,9 @@ namespace hda {
 cudaError_t launch_gemm_simt(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                              const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
                              cudaStream_t s);
+cudaError_t launch_gemm_2sm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                            const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
+                            cudaStream_t s);
 
 namespace tc {
 
@@ -397,6 +401,15 @@ cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int6
                         cudaStream_t s) {
   const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
   if (m0 >= m1 || n0 >= n1) return cudaSuccess;
+  // CTA-pair kernel (gemm_tcgen05_2sm.cu) when HDA_GEMM_2SM=1
+  static const int two_sm = [] {
+    const char* e = std::getenv("HDA_GEMM_2SM");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (two_sm) {
+    const cudaError_t e = launch_gemm_2sm(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, ks, s);
+    if (e != cudaErrorNotSupported) return e;
+  }
   // TMA needs 16-byte row pitches and aligned bases; tiny problems use the CUDA-core path
   const bool tc_ok = (K % 8 == 0) && (N % 8 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) &&
                      K >= tc::BK && N >= 64 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX;

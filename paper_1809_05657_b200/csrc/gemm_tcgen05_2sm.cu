@@ -1,0 +1,414 @@
+// gemm_tcgen05_2sm.cu — the product of Listing 2 on CTA pairs:
+// tcgen05.mma.cta_group::2, M=256 (128 rows per CTA) x N=256 x K=16, so each SM
+// stages A for its own 128 rows and only HALF of B (128 columns): 32 KiB per stage per
+// CTA instead of 48, one third less L2->SM traffic than the single-CTA kernel.
+//
+// Cluster of 2 CTAs (one per SM of a TPC), persistent over 256x256 tiles:
+//   warp 0  TMA producer (both CTAs): A 128x64 + B 64x128 per stage into its own smem,
+//           completion counted on the LEADER's full barrier (.cta_group::2 TMA)
+//   warp 1  MMA issuer (leader CTA only), commits multicast to both CTAs' barriers
+//   warp 2  TMEM allocator (both CTAs, .cta_group::2, 2 x 256 columns)
+//   warps 4-7  epilogue (both CTAs): each CTA drains its 128 rows of the accumulator
+// Every mbarrier wait is bounded; a timeout aborts the whole grid quickly (wrong
+// results, caught by the parity tests) instead of hanging the GPU.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.cuh"
+#include "sync.cuh"
+
+namespace hda {
+namespace tc2 {
+
+constexpr int BM = 128;   // rows per CTA (the pair covers 256)
+constexpr int BN = 256;   // accumulator columns (each CTA stages 128 of B)
+constexpr int BNH = 128;  // B columns staged per CTA
+constexpr int BK = 64, UK = 16;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;            // 16 KiB
+constexpr int B_BYTES = BK * BNH * 2;           // 16 KiB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KiB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int THREADS = 256;
+constexpr int TMEM_COLS = 512;
+
+__device__ int g_abort = 0;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ bool aborted() { return *reinterpret_cast<volatile int*>(&g_abort) != 0; }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!aborted()) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (1LL << 32)) {  // ~2 s: a protocol bug; stop the grid
+      atomicExch(&g_abort, 1);
+      return;
+    }
+  }
+}
+
+// TMA into this CTA's smem, completion bytes counted on `bar` (the leader's barrier)
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+// D f32, A/B bf16, A K-major, B MN-major, M = 256 (the pair), N = 256
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)((2 * BM) >> 4) << 24);
+
+__device__ __forceinline__ void mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+// arrive on the barrier at this smem offset in BOTH CTAs once the MMAs issued so far complete
+__device__ __forceinline__ void commit_both(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <typename TC>
+__device__ __forceinline__ void store32(TC* row, int64_t col0, int64_t n0, int64_t n1, const uint32_t (&r)[32],
+                                        float alpha, float beta) {
+  for (int j = 0; j < 32; j++) {
+    const int64_t c = col0 + j;
+    if (c < n0 || c >= n1) continue;
+    float v = alpha * __uint_as_float(r[j]);
+    if (beta != 0.f) v = fmaf(beta, (float)row[c], v);
+    row[c] = (TC)v;
+  }
+}
+template <>
+__device__ __forceinline__ void store32<float>(float* row, int64_t col0, int64_t n0, int64_t n1,
+                                               const uint32_t (&r)[32], float alpha, float beta) {
+  if (col0 >= n0 && col0 + 32 <= n1 && ((uintptr_t)(row + col0) % 16 == 0)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float4 v = make_float4(alpha * __uint_as_float(r[j]), alpha * __uint_as_float(r[j + 1]),
+                             alpha * __uint_as_float(r[j + 2]), alpha * __uint_as_float(r[j + 3]));
+      float4* p = reinterpret_cast<float4*>(row + col0 + j);
+      if (beta != 0.f) {
+        const float4 c = *p;
+        v.x = fmaf(beta, c.x, v.x);
+        v.y = fmaf(beta, c.y, v.y);
+        v.z = fmaf(beta, c.z, v.z);
+        v.w = fmaf(beta, c.w, v.w);
+      }
+      *p = v;
+    }
+    return;
+  }
+  for (int j = 0; j < 32; j++) {
+    const int64_t c = col0 + j;
+    if (c < n0 || c >= n1) continue;
+    float v = alpha * __uint_as_float(r[j]);
+    if (beta != 0.f) v = fmaf(beta, row[c], v);
+    row[c] = v;
+  }
+}
+template <>
+__device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* row, int64_t col0, int64_t n0, int64_t n1,
+                                                       const uint32_t (&r)[32], float alpha, float beta) {
+  for (int j = 0; j < 32; j++) {
+    const int64_t c = col0 + j;
+    if (c < n0 || c >= n1) continue;
+    float v = alpha * __uint_as_float(r[j]);
+    if (beta != 0.f) v = fmaf(beta, __bfloat162float(row[c]), v);
+    row[c] = __float2bfloat16_rn(v);
+  }
+}
+
+constexpr int GROUP_M = 8;  // 256-row tiles per group (grouped raster, L2 reuse)
+__device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n, int& mt, int& nt) {
+  const int64_t per_group = (int64_t)GROUP_M * tiles_n;
+  const int64_t g = t / per_group, local = t - g * per_group;
+  const int64_t rows = min((int64_t)GROUP_M, tiles_m - g * GROUP_M);
+  mt = (int)(g * GROUP_M + local % rows);
+  nt = (int)(local / rows);
+}
+
+template <typename TC>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, TC* C,
+                 int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, float alpha, float beta,
+                 const __grid_constant__ KSync ks) {
+  ks_pre(ks);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2] (leader's are the ones used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int64_t tiles_m = (m1 - m0 + 2 * BM - 1) / (2 * BM), tiles_n = (n1 - n0 + BN - 1) / BN;
+  const int64_t n_tiles = tiles_m * tiles_n;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int kblocks = (int)((K + BK - 1) / BK);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);   // the leader's producer arrives (expect_tx of both CTAs)
+      mbar_init(&empty[s], 1);  // one multicast commit per use
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's barrier)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 2) {  // same warp in both CTAs (joint allocation)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      const uint32_t full0 = mapa(smem_u32(&full[0]), 0);  // the leader's full[0]
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
+        int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, mt, nt);
+        const int row0 = (int)(m0 + (int64_t)mt * 2 * BM + rank * BM);
+        const int col0 = (int)(n0 + (int64_t)nt * BN + rank * BNH);
+        for (int kb = 0; kb < kblocks && !aborted(); kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+          tma_load_2sm(sa, &map_a, fb, kb * BK, row0);
+#pragma unroll
+          for (int j = 0; j < BNH / 64; j++) tma_load_2sm(sb + j * (BK * 128), &map_b, fb, col0 + 64 * j, kb * BK);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < kblocks && !aborted(); kb++) {
+          mbar_wait(&full[s], ph);
+          fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / UK; k++) {
+            const uint64_t ad = smem_desc(a_addr + k * (UK * 2), 16, 1024);
+            const uint64_t bd = smem_desc(b_addr + k * (UK * 128), BK * 128, 1024);
+            mma2(tmem_d, ad, bd, (kb | k) != 0);
+          }
+          commit_both(&empty[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        commit_both(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue (both CTAs; TMEM lane quarter = warp % 4)
+    const int q = warp % 4;
+    const uint32_t tempty0 = mapa(smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
+      int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, mt, nt);
+      const int64_t row = m0 + (int64_t)mt * 2 * BM + rank * BM + q * 32 + lane;
+      const int64_t colb = n0 + (int64_t)nt * BN;
+      mbar_wait(&tfull[acc], aph);
+      fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; c++) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c * 32, r);
+        if (row < m1) store32<TC>(C + row * N, colb + c * 32, n0, n1, r, alpha, beta);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  if (warp == 2) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
+  }
+  ks_post(ks);
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled get_encode() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiled)p;
+  });
+  return fn;
+}
+static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename TC>
+static cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, TC* C, int64_t N, int64_t K, int64_t m0,
+                            int64_t m1, int64_t n0, int64_t n1, float alpha, float beta, const KSync& ks,
+                            cudaStream_t s, int sms) {
+  const int64_t tiles = ((m1 - m0 + 2 * BM - 1) / (2 * BM)) * ((n1 - n0 + BN - 1) / BN);
+  const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms / 2));
+  cudaFuncSetAttribute(gemm2_kernel<TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm2_kernel<TC>, ma, mb, C, N, K, m0, m1, n0, n1, alpha, beta, ks);
+}
+
+}  // namespace tc2
+
+// Returns cudaErrorNotSupported when the 2-SM path does not apply (caller falls back).
+cudaError_t launch_gemm_2sm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
+                            const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
+                            cudaStream_t s) {
+  const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
+  const bool ok = (K % 8 == 0) && (N % 8 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) &&
+                  K >= tc2::BK && N >= 128 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX &&
+                  (m1 - m0) >= 2 * tc2::BM;
+  CUtensorMap ma, mb;
+  if (!ok || !tc2::make_map(&ma, A, (uint64_t)K, (uint64_t)M, tc2::BM) ||
+      !tc2::make_map(&mb, B, (uint64_t)N, (uint64_t)K, tc2::BK))
+    return cudaErrorNotSupported;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (c_dtype == 1)
+    return tc2::launch_t<float>(ma, mb, (float*)C, N, K, m0, m1, n0, n1, alpha, beta, ks, s, sms);
+  return tc2::launch_t<__nv_bfloat16>(ma, mb, (__nv_bfloat16*)C, N, K, m0, m1, n0, n1, alpha, beta, ks, s, sms);
+}
+
+}  // namespace hda
