@@ -62,21 +62,35 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// bounded wait; the abort flag (a global load) is polled only while a wait is slow,
+// never on the fast path.  CLUSTER: acquire at cluster scope (remote arrivals).
+template <bool CLUSTER = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  const long long t0 = clock64();
-  while (!aborted()) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
+  uint32_t ok = 0;
+  for (int spin = 0;; spin++) {
+    if (CLUSTER)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(ok)
+          : "r"(smem_u32(b)), "r"(parity)
+          : "memory");
+    else
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(ok)
+          : "r"(smem_u32(b)), "r"(parity)
+          : "memory");
     if (ok) return;
-    if (clock64() - t0 > (1LL << 32)) {  // ~2 s: a protocol bug; stop the grid
-      atomicExch(&g_abort, 1);
-      return;
+    if ((spin & 1023) == 1023) {
+      if (aborted()) return;
+      if (spin > (1 << 22)) {  // seconds: a protocol bug; stop the grid
+        atomicExch(&g_abort, 1);
+        return;
+      }
     }
   }
 }
@@ -247,12 +261,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t full0 = mapa(smem_u32(&full[0]), 0);  // the leader's full[0]
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
+      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {  // abort checked per tile only
         int mt, nt;
         tile_coords(t, tiles_m, tiles_n, mt, nt);
         const int row0 = (int)(m0 + (int64_t)mt * 2 * BM + rank * BM);
         const int col0 = (int)(n0 + (int64_t)nt * BN + rank * BNH);
-        for (int kb = 0; kb < kblocks && !aborted(); kb++) {
+        for (int kb = 0; kb < kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -275,10 +289,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       int acc = 0;
       uint32_t aph = 0;
       for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
-        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait<true>(&tempty[acc], aph ^ 1);  // arrivals from both CTAs' epilogues
         fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < kblocks && !aborted(); kb++) {
+        for (int kb = 0; kb < kblocks; kb++) {
           mbar_wait(&full[s], ph);
           fence_after();
           const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
