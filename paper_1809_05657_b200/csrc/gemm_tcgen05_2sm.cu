@@ -29,7 +29,13 @@ constexpr int BM = 128;   // rows per CTA (the pair covers 256)
 constexpr int BN = 256;   // accumulator columns (each CTA stages 128 of B)
 constexpr int BNH = 128;  // B columns staged per CTA
 constexpr int BK = 64, UK = 16;
-constexpr int STAGES = 6;
+#ifndef GEMM2_STAGES
+#define GEMM2_STAGES 6
+#endif
+#ifndef GEMM2_GROUP_M
+#define GEMM2_GROUP_M 8
+#endif
+constexpr int STAGES = GEMM2_STAGES;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KiB
 constexpr int B_BYTES = BK * BNH * 2;           // 16 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // 32 KiB
@@ -193,6 +199,29 @@ __device__ __forceinline__ void store32<float>(float* row, int64_t col0, int64_t
 template <>
 __device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* row, int64_t col0, int64_t n0, int64_t n1,
                                                        const uint32_t (&r)[32], float alpha, float beta) {
+  if (col0 >= n0 && col0 + 32 <= n1 && ((uintptr_t)(row + col0) % 16 == 0)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      uint4* p = reinterpret_cast<uint4*>(row + col0 + j);
+      float c[8];
+      if (beta != 0.f) {
+        const uint4 cv = *p;
+        const __nv_bfloat16* cb = reinterpret_cast<const __nv_bfloat16*>(&cv);
+#pragma unroll
+        for (int t = 0; t < 8; t++) c[t] = __bfloat162float(cb[t]);
+      }
+      uint4 out;
+      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&out);
+#pragma unroll
+      for (int t = 0; t < 8; t++) {
+        float v = alpha * __uint_as_float(r[j + t]);
+        if (beta != 0.f) v = fmaf(beta, c[t], v);
+        ob[t] = __float2bfloat16_rn(v);
+      }
+      *p = out;
+    }
+    return;
+  }
   for (int j = 0; j < 32; j++) {
     const int64_t c = col0 + j;
     if (c < n0 || c >= n1) continue;
@@ -202,7 +231,7 @@ __device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* row, int64
   }
 }
 
-constexpr int GROUP_M = 8;  // 256-row tiles per group (grouped raster, L2 reuse)
+constexpr int GROUP_M = GEMM2_GROUP_M;  // 256-row tiles per group (grouped raster, L2 reuse)
 __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t tiles_n, int& mt, int& nt) {
   const int64_t per_group = (int64_t)GROUP_M * tiles_n;
   const int64_t g = t / per_group, local = t - g * per_group;
