@@ -358,7 +358,7 @@ class Gemm:
         self.acc = [(self.C, [], [(0, 0)]), (self.A, [(0, S)], []), (self.B, [(S, 0)], [])]
         self.kind = "gemm"
         self.workload = f"configs[4] (product half): {n}^2 bf16 GEMM, fp32 accumulate and C, ROW partition, B use=all"
-        self.kname = "gemm_kernel<float> (tcgen05)"
+        self.kname = "gemm2_kernel<float> (tcgen05 cta_group::2)"
         self.dtype_name = "bf16"
         self.metric_unit = "TFLOP/s"
         self.bound = "tensor"
@@ -650,11 +650,13 @@ def main():
             burst, sustained = float(mp["bf16_tflops"]), float(mp["bf16_tflops_sustained"])
         except Exception:
             pass
-        # the tcgen05 kernel runs above cuBLAS's back-to-back "sustained" figure, so the
-        # burst figure (the larger) is the denominator; the sustained ratio rides along
+        # the denominator is the measured cuBLAS burst figure (MEASURED_PEAKS.json, an 8192^3
+        # torch.matmul); the CTA-pair kernel at 16384^3 can exceed it (frac > 1), so the
+        # ratio to the nominal dense peak (2.25 PFLOP/s) rides along
         achieved = wl.alg_per_launch / (k_avg * 1e-3) / 1e12
         roof = {"bound": "tensor", "kernel": wl.kname, "achieved": achieved, "peak": burst, "unit": "TFLOP/s",
                 "frac": achieved / burst, "frac_of_sustained": achieved / sustained,
+                "frac_of_nominal_dense_2250": achieved / 2250.0,
                 "peak_source": "measured cuBLAS bf16 burst (MEASURED_PEAKS.json); sustained 1399.6",
                 "algorithmic_flops_per_launch": wl.alg_per_launch, "avg_launch_ms": k_avg}
     if ws > 1:
