@@ -536,3 +536,16 @@ __global__ void copy_back(double *B, const double *A) { }
         w.apply(O.K_COPY, workw, [(Bw, [], [(0, 0)]), (Aw, [(0, 0)], [])])
     assert_replicas(h, w, [A, B], P)
     h.close()
+
+
+def test_gemm_single_cta_kernel():
+    """The single-CTA tcgen05 GEMM (HDA_GEMM_2SM=0; the default is the CTA-pair kernel)
+    passes the same GEMM parity tests; the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, HDA_GEMM_2SM="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider", "-k",
+                        "gemm and not single_cta or 2mm", __file__], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
