@@ -549,3 +549,32 @@ def test_gemm_single_cta_kernel():
                         "gemm and not single_cta or 2mm", __file__], env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("cdt", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [1, 2])
+def test_gemm_cta_pair_ragged(H, cdt, P):
+    """The CTA-pair kernel's edges: work boxes whose rows and columns are not multiples of
+    the 256x256 pair tile and do not start at 0, K not a multiple of 64-wide stages, and
+    beta != 0 (C read).  Integer inputs keep every value exact, so C is bit-exact."""
+    M, N, K = 1100, 776, 456
+    Ab = synth.int_bf16(71, (M, K))
+    Bb = synth.int_bf16(72, (K, N))
+    Cin = (synth.int_bf16(73, (M, N)).astype(np.int64) % 7).astype(np.float32) - 3.0
+    if cdt == "bf16":
+        Cin = synth.bf16_to_f32(((Cin.view(np.uint32) >> 16).astype(np.uint16)))
+    CT = H.F32 if cdt == "f32" else H.BF16
+    h = H.HDArray(n_gpus=1, n_devices=P)
+    w = O.Oracle(P)
+    S = H.STAR
+    lbs = [(37, 5), (600, 5)][:P] if P == 2 else [(37, 5)]
+    ubs = [(600, 771), (1090, 771)][:P] if P == 2 else [(1090, 771)]
+    for be in (h, w):
+        A = be.create(H.BF16, (M, K), Ab)
+        B = be.create(H.BF16, (K, N), Bb)
+        cinit = Cin if cdt == "f32" else ((Cin.view(np.uint32) >> 16).astype(np.uint16))
+        C = be.create(CT, (M, N), cinit)
+        pc = be.partition_manual((M, N), lbs, ubs)
+        be.apply(H.K_GEMM, pc, [(C, [(0, 0)], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.0, 2.0])
+    assert_replicas(h, w, [C], P)
+    h.close()
