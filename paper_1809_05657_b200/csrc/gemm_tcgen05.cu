@@ -216,8 +216,8 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t 
 template <typename TC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, TC* C,
-                int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, float alpha, float beta,
-                const __grid_constant__ KSync ks) {
+                int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, int64_t nbase, float alpha,
+                float beta, const __grid_constant__ KSync ks) {
   ks_pre(ks);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t tiles_m = (m1 - m0 + BM - 1) / BM, tiles_n = (n1 - n0 + BN - 1) / BN;
+  const int64_t tiles_m = (m1 - m0 + BM - 1) / BM, tiles_n = (n1 - nbase + BN - 1) / BN;
   const int64_t n_tiles = tiles_m * tiles_n;
   const int kblocks = (int)((K + BK - 1) / BK);
 
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         int mt, nt;
         tile_coords(t, tiles_m, tiles_n, mt, nt);
-        const int row0 = (int)(m0 + (int64_t)mt * BM), col0 = (int)(n0 + (int64_t)nt * BN);
+        const int row0 = (int)(m0 + (int64_t)mt * BM), col0 = (int)(nbase + (int64_t)nt * BN);
         for (int kb = 0; kb < kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int mt, nt;
       tile_coords(t, tiles_m, tiles_n, mt, nt);
       const int64_t row = m0 + (int64_t)mt * BM + q * 32 + lane;
-      const int64_t colb = n0 + (int64_t)nt * BN;
+      const int64_t colb = nbase + (int64_t)nt * BN;
       mbar_wait(&tfull[acc], aph);
       fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
@@ -418,17 +418,21 @@ cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int6
   if (!tc_ok || !tc::make_map(&ma, A, (uint64_t)K, (uint64_t)M, tc::BM) ||
       !tc::make_map(&mb, B, (uint64_t)N, (uint64_t)K, tc::BK))
     return launch_gemm_simt(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, ks, s);
-  const int64_t tiles = ((m1 - m0 + tc::BM - 1) / tc::BM) * ((n1 - n0 + tc::BN - 1) / tc::BN);
+  // TMA inner coordinates must be 16-byte aligned (measured: an odd column offset traps
+  // as an illegal instruction): tiles start at n0 rounded down to 8 columns, stores
+  // still skip columns below n0
+  const int64_t nbase = n0 & ~(int64_t)7;
+  const int64_t tiles = ((m1 - m0 + tc::BM - 1) / tc::BM) * ((n1 - nbase + tc::BN - 1) / tc::BN);
   const int grid = (int)std::min<int64_t>(tiles, sm_count());
   if (c_dtype == 1) {
     cudaFuncSetAttribute(tc::gemm_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-    tc::gemm_kernel<float><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(ma, mb, (float*)C, N, K, m0, m1, n0, n1, alpha,
-                                                                     beta, ks);
+    tc::gemm_kernel<float><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(ma, mb, (float*)C, N, K, m0, m1, n0, n1, nbase,
+                                                                     alpha, beta, ks);
   } else {
     cudaFuncSetAttribute(tc::gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          tc::SMEM_BYTES);
     tc::gemm_kernel<__nv_bfloat16><<<grid, tc::THREADS, tc::SMEM_BYTES, s>>>(ma, mb, (__nv_bfloat16*)C, N, K, m0,
-                                                                             m1, n0, n1, alpha, beta, ks);
+                                                                             m1, n0, n1, nbase, alpha, beta, ks);
   }
   return cudaGetLastError();
 }

@@ -243,8 +243,8 @@ __device__ __forceinline__ void tile_coords(int64_t t, int64_t tiles_m, int64_t 
 template <typename TC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, TC* C,
-                 int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, float alpha, float beta,
-                 const __grid_constant__ KSync ks) {
+                 int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, int64_t nbase, float alpha,
+                 float beta, const __grid_constant__ KSync ks) {
   ks_pre(ks);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
-  const int64_t tiles_m = (m1 - m0 + 2 * BM - 1) / (2 * BM), tiles_n = (n1 - n0 + BN - 1) / BN;
+  const int64_t tiles_m = (m1 - m0 + 2 * BM - 1) / (2 * BM), tiles_n = (n1 - nbase + BN - 1) / BN;
   const int64_t n_tiles = tiles_m * tiles_n;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int kblocks = (int)((K + BK - 1) / BK);
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int mt, nt;
         tile_coords(t, tiles_m, tiles_n, mt, nt);
         const int row0 = (int)(m0 + (int64_t)mt * 2 * BM + rank * BM);
-        const int col0 = (int)(n0 + (int64_t)nt * BN + rank * BNH);
+        const int col0 = (int)(nbase + (int64_t)nt * BN + rank * BNH);
         for (int kb = 0; kb < kblocks; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int mt, nt;
       tile_coords(t, tiles_m, tiles_n, mt, nt);
       const int64_t row = m0 + (int64_t)mt * 2 * BM + rank * BM + q * 32 + lane;
-      const int64_t colb = n0 + (int64_t)nt * BN;
+      const int64_t colb = nbase + (int64_t)nt * BN;
       mbar_wait(&tfull[acc], aph);
       fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
@@ -414,7 +414,8 @@ template <typename TC>
 static cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, TC* C, int64_t N, int64_t K, int64_t m0,
                             int64_t m1, int64_t n0, int64_t n1, float alpha, float beta, const KSync& ks,
                             cudaStream_t s, int sms) {
-  const int64_t tiles = ((m1 - m0 + 2 * BM - 1) / (2 * BM)) * ((n1 - n0 + BN - 1) / BN);
+  const int64_t nbase = n0 & ~(int64_t)7;  // 16-byte aligned TMA column base (see gemm_tcgen05.cu)
+  const int64_t tiles = ((m1 - m0 + 2 * BM - 1) / (2 * BM)) * ((n1 - nbase + BN - 1) / BN);
   const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms / 2));
   cudaFuncSetAttribute(gemm2_kernel<TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   cudaLaunchConfig_t cfg = {};
@@ -429,7 +430,7 @@ static cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, TC* C,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm2_kernel<TC>, ma, mb, C, N, K, m0, m1, n0, n1, alpha, beta, ks);
+  return cudaLaunchKernelEx(&cfg, gemm2_kernel<TC>, ma, mb, C, N, K, m0, m1, n0, n1, nbase, alpha, beta, ks);
 }
 
 }  // namespace tc2
