@@ -347,6 +347,7 @@ struct Boxes2 {
   int64_t tstart[9];  // flat-grid launches: first tile of each box
   int32_t gx[8], gy[8];
   int32_t n;
+  int32_t ndep_first;  // fused halo kernel: boxes [0, ndep_first) are the boundary strips
 };
 
 template <typename T, int KIND, int ROWS, bool CG>
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs t
   int b;
   int64_t xb, yb;
   tile_of(bx, bid - pp.nblocks, b, xb, yb);
-  if (b >= n_interior) {
+  if (bx.ndep_first ? b < bx.ndep_first : b >= n_interior) {
     if (threadIdx.x == 0) {
       const unsigned long long t0 = ks_timer();
       while (ks_ld_acquire(pp.done_word) < pp.epoch) {
@@ -596,6 +597,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     constexpr int ROWS = ST_ROWS;
     Boxes2 bx;
     bx.n = 0;
+    bx.ndep_first = 0;
     for (int i = 0; i < nb && bx.n < 8; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
       if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
@@ -725,7 +727,15 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     tiles16 += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
     if (k < ni && bx.c1[k] - bx.c0[k] > 64) strips_i += bx.gx[k];
   }
-  const bool one_wave = one_wave_enabled() && tiles16 < 5 * wave && strips_i > 0 && wave - npull >= strips_i;
+  // HDA_DEP_FIRST (default 1): the boundary strips are dispatched right after the pull
+  // blocks instead of last, so the step ends with interior tiles only (as a standalone
+  // launch) instead of the strips' wait + compute latency
+  static const int dep_first = env_or("HDA_DEP_FIRST", 1);
+  int64_t dep_tiles = 0;
+  for (int k = ni; k < bx.n; k++)
+    dep_tiles += (int64_t)bx.gx[k] * ((bx.r1[k] - bx.r0[k] + ST_ROWS - 1) / ST_ROWS);
+  const int64_t slots = wave - npull - (dep_first ? dep_tiles : 0);
+  const bool one_wave = one_wave_enabled() && tiles16 < 5 * wave && strips_i > 0 && slots >= strips_i;
   // many-wave share (N=2) with one interior box: its last rows as a tail box of short
   // tiles, dispatched after the interior and before the boundary strips (5-point only,
   // as in the plain launch)
@@ -760,13 +770,29 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     const int64_t rows = bx.r1[k] - bx.r0[k];
     int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
     if (one_wave && k < ni && bx.c1[k] - bx.c0[k] > 64) {
-      gyk = std::max<int64_t>(1, (wave - npull) / strips_i);
+      gyk = std::max<int64_t>(1, slots / strips_i);
       gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
     }
     if (k == tail_k) gyk = (rows + tail_rows() - 1) / tail_rows();  // short tiles
     bx.rpb[k] = (rows + gyk - 1) / gyk;
     bx.gy[k] = (int)((rows + bx.rpb[k] - 1) / bx.rpb[k]);
     bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
+  }
+  bx.ndep_first = 0;
+  if (dep_first && ni < bx.n) {  // rotate the boundary boxes to the front
+    Boxes2 o = bx;
+    int j = 0;
+    for (int k = ni; k < o.n; k++, j++) {
+      bx.r0[j] = o.r0[k], bx.r1[j] = o.r1[k], bx.c0[j] = o.c0[k], bx.c1[j] = o.c1[k];
+      bx.cbase[j] = o.cbase[k], bx.rpb[j] = o.rpb[k], bx.gx[j] = o.gx[k], bx.gy[j] = o.gy[k];
+    }
+    for (int k = 0; k < ni; k++, j++) {
+      bx.r0[j] = o.r0[k], bx.r1[j] = o.r1[k], bx.c0[j] = o.c0[k], bx.c1[j] = o.c1[k];
+      bx.cbase[j] = o.cbase[k], bx.rpb[j] = o.rpb[k], bx.gx[j] = o.gx[k], bx.gy[j] = o.gy[k];
+    }
+    bx.ndep_first = o.n - ni;
+    bx.tstart[0] = 0;
+    for (int k = 0; k < bx.n; k++) bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
   }
   PullPart pp;
   std::memset(&pp, 0, sizeof pp);
