@@ -691,6 +691,25 @@ def main():
 
     par = wl.parity()
 
+    # context for the tensor roofline: cuBLAS (torch.matmul) on the same shape, same GPU
+    cublas = None
+    if isinstance(wl, (Gemm, TwoMM)) and ws == 1:
+        a = torch.randn(wl.n, wl.n, device="cuda", dtype=torch.bfloat16)
+        b = torch.randn(wl.n, wl.n, device="cuda", dtype=torch.bfloat16)
+        for _ in range(3):
+            torch.matmul(a, b)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        reps = 10
+        for _ in range(reps):
+            torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        cublas = 2.0 * wl.n ** 3 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12
+        roof["cublas_same_shape_tflops"] = cublas
+        del a, b
+
     # ---- end to end through the C-ABI with host buffers (stencils: write (pinned H2D)
     # -> e2e_sweeps sweeps -> read (D2H) per job)
     e2e = None
