@@ -484,7 +484,10 @@ struct PullPart {
 };
 
 template <typename T, int KIND, int ROWS>
-__global__ void __launch_bounds__(ST_THREADS, ST_MINB)  // the pull role needs the registers of minB 4
+#ifndef HALO_MINB0
+#define HALO_MINB0 4  // 5-point fused kernel: CTAs per SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(ST_THREADS, KIND == 0 ? HALO_MINB0 : ST_MINB)
     stencil2d_halo_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
                           const __grid_constant__ Boxes2 bx, int32_t n_interior,
                           const __grid_constant__ RunBatch pull, const __grid_constant__ PullPart pp,
