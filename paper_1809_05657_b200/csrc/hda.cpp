@@ -207,6 +207,12 @@ struct hda_ctx {
   unsigned long long epoch = 0;
   std::vector<unsigned long long> last_prod;
   std::vector<std::vector<std::vector<unsigned long long>>> pend;  // [array][src][dst]
+  // [array][dev]: boxes peers pulled from dev's replica since dev last wrote the array
+  // (per-box WAR: kernel parts disjoint from them need no WAR wait); over => unknown
+  std::vector<std::vector<std::vector<Box>>> rread;
+  std::vector<std::vector<char>> rread_over;
+  std::vector<int> split_mode;  // per device: 2 = this call's boundary part ran on the comm stream
+  std::vector<char> war_done;   // per device: WAR waits already issued for this call
   std::vector<std::vector<std::pair<int, unsigned long long>>> stage_pend;  // [src]
   std::vector<char*> send_stage, recv_stage;
   std::vector<size_t> send_cap, recv_cap;
@@ -682,12 +688,29 @@ static int exchange_plan(hda_ctx_t* ctx, const Transition* t, unsigned long long
   }
   if (!ep->staged)
     for (const PendEntry& e : ep->reads) ctx->pend[e.array][e.src][e.dst] = k;
+  for (const Msg& m : t->msgs) {
+    if (same_stream(ctx, m.src, m.dst)) continue;
+    auto& v = ctx->rread[m.array][m.src];
+    if (v.size() >= 32) {
+      ctx->rread_over[m.array][m.src] = 1;
+    } else {
+      bool dup = false;
+      for (const Box& b : v) dup = dup || box_eq(b, m.box);
+      if (!dup) v.push_back(m.box);
+    }
+  }
   *out = ep;
   return HDA_OK;
 }
 
+static void war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q, KSync& ks);
+static bool war_disjoint(hda_ctx_t* ctx, const CallInfo& ci, int q, const std::vector<Box>& boxes);
+static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
+                      const std::vector<Box>* boxes = nullptr, cudaStream_t stream = nullptr);
+
 // one device's pull (reader q = job.dst): thread-safe against the other devices' issue
-static int issue_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k, bool overlap_kernel, bool halo_kernel) {
+static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigned long long k, bool overlap_kernel,
+                      bool halo_kernel, const double* scalars) {
   const int q = job.dst;
   CK(cudaSetDevice(ordinal_of(ctx, q)));
   Gpu& g = ctx->gpus[ctx->dev[q].gpu];
@@ -699,6 +722,22 @@ static int issue_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k, bool o
   }
   const bool comm = ctx->overlap && job.cross && job.split && overlap_kernel;
   cudaStream_t st = comm ? g.comm : g.stream;
+  // Stencils on the comm path: when the interior part touches no cell a peer pulled
+  // from this replica (per-box WAR), the pull carries the WAR waits and the boundary
+  // part runs on the comm stream right after it; the main stream runs the interior with
+  // no waits and only joins before the PROD signal (HDA_COMM_BOUNDARY=0: boundary after
+  // the interior on the main stream)
+  static const int comm_boundary = env_int("HDA_COMM_BOUNDARY", 1);
+  static const int sig_kernel_on = env_int("HDA_SIG_KERNEL", 1);
+  const CallInfo& ci = *t->info;
+  const bool stencil = ci.kernel == KN_JACOBI5 || ci.kernel == KN_STENCIL9 || ci.kernel == KN_STENCIL7_3D;
+  const bool boundary_on_comm = comm && comm_boundary && sig_kernel_on && stencil && !job.interior.empty() &&
+                                !job.dependent.empty() && war_disjoint(ctx, ci, q, job.interior);
+  KSync war = ks_empty(ctx);
+  if (boundary_on_comm) {
+    war_waits(ctx, ci, q, war);
+    ctx->war_done[q] = 1;
+  }
   if (comm) {  // the pull may start as soon as everything issued before this call is done
     CK(cudaEventRecord(g.ev_fork, g.stream));
     CK(cudaStreamWaitEvent(g.comm, g.ev_fork, 0));
@@ -714,6 +753,7 @@ static int issue_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k, bool o
       ks_wait(pre, ctx->dev[q].sync + SW_PROD + p, ctx->last_prod[p]);
       ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
     }
+  for (int i = 0; i < war.nwait; i++) ks_wait(pre, war.wait_ptr[i], war.wait_val[i]);
   int rc;
   cudaEvent_t a = nullptr;
   const size_t nb = job.batches.size();
@@ -757,6 +797,14 @@ static int issue_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k, bool o
   }
   mark(ctx, q, 0);
   if ((rc = timed_end(ctx, st, -100, a))) return rc;
+  if (boundary_on_comm) {
+    cudaEvent_t b;
+    if ((rc = timed_begin(ctx, g.comm, &b))) return rc;
+    if ((rc = run_kernel(ctx, t, q, scalars, ks_empty(ctx), &job.dependent, g.comm))) return rc;
+    mark(ctx, q, 3);
+    if ((rc = timed_end(ctx, g.comm, ci.kernel, b, 0))) return rc;
+    ctx->split_mode[q] = 2;
+  }
   if (comm) CK(cudaEventRecord(g.ev_pull, g.comm));
   return HDA_OK;
 }
@@ -831,7 +879,23 @@ static void war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q, KSync& ks) {
       if (row[r] && !same_stream(ctx, q, r)) ks_wait(ks, ctx->dev[q].sync + SW_ACK + r, row[r]);
       row[r] = 0;
     }
+    ctx->rread[ci.arrays[i]][q].clear();
+    ctx->rread_over[ci.arrays[i]][q] = 0;
   }
+}
+
+// true if no box in `boxes` touches a cell peers pulled from q's copy of an array q
+// defines in this call (since q last wrote it): writing them needs no WAR wait
+static bool war_disjoint(hda_ctx_t* ctx, const CallInfo& ci, int q, const std::vector<Box>& boxes) {
+  for (size_t i = 0; i < ci.arrays.size(); i++) {
+    if (ci.ldef[i][q].empty()) continue;
+    const int a = ci.arrays[i];
+    if (ctx->rread_over[a][q]) return false;
+    for (const Box& r : ctx->rread[a][q])
+      for (const Box& b : boxes)
+        if (!box_empty(box_and(r, b))) return false;
+  }
+  return true;
 }
 
 // RAW: publish "device q completed call k" to every peer
@@ -871,7 +935,7 @@ static KSync ks_part(hda_ctx_t* ctx, const KSync& ks, bool first, bool last) {
 }
 
 static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
-                      const std::vector<Box>* boxes = nullptr) {
+                      const std::vector<Box>* boxes, cudaStream_t stream) {
   const CallInfo& ci = *t->info;
   const TPart& pt = ctx->tr->part(ci.part);
   const int X0 = ci.param_array[0];
@@ -885,7 +949,7 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
     fbs.push_back(front_box(a0.ndim, pt.box[q]));
   }
   const Box fb = fbs.empty() ? front_box(a0.ndim, pt.box[q]) : fbs[0];
-  cudaStream_t s = stream_of(ctx, q);
+  cudaStream_t s = stream ? stream : stream_of(ctx, q);
   auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
   if (ci.kernel == KN_JACOBI5 || ci.kernel == KN_STENCIL9) {
     const size_t nb = fbs.size();
@@ -909,7 +973,7 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
   if (fbs.size() > 1 && (ci.kernel == KN_STENCIL7_3D || ci.kernel == KN_SCALE || ci.kernel == KN_COPY)) {
     for (size_t i = 0; i < fbs.size(); i++) {
       std::vector<Box> one{boxes->at(i)};
-      int rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, i == 0, i + 1 == fbs.size()), &one);
+      int rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, i == 0, i + 1 == fbs.size()), &one, stream);
       if (rc) return rc;
     }
     return HDA_OK;
@@ -1048,7 +1112,8 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
   CK(cudaSetDevice(ordinal_of(ctx, q)));
   KSync ks = ks_empty(ctx);
   if (defines) {
-    war_waits(ctx, ci, q, ks);
+    if (!ctx->war_done[q]) war_waits(ctx, ci, q, ks);  // else: carried by the pull
+    ctx->war_done[q] = 0;
     signal_prod(ctx, q, k, ks);
     // HDA_DEBUG_FAKE_SIGNAL=1: a kernel with no peer to signal still runs the
     // end-of-kernel fence + counter + store (to a local word) — measures their cost
@@ -1153,6 +1218,17 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
     Gpu& g = ctx->gpus[ctx->dev[q].gpu];
     bool joined = false;
     const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
+    if (ctx->split_mode[q] == 2) {  // boundary already issued on the comm stream
+      ctx->split_mode[q] = 0;
+      cudaEvent_t a;
+      if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+      if ((rc = run_kernel(ctx, t, q, scalars, ks, &job.interior))) return rc;
+      mark(ctx, q, 2);
+      if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
+      CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+      ctx->pulled_on_comm[q] = 0;
+      goto kernel_done;
+    }
     if (ks.nwait > 0) {
       // The peers' pulls this WAR wait depends on need SM time (their pull kernels)
       // or stall behind GPU-filling kernels (measured: cross-process 3-D peer copies
@@ -1193,6 +1269,7 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
   } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
     return rc;
   }
+kernel_done:
   if (split_sig) {
     CK(launch_signal_pdl(post_sig, ks.relaxed, stream_of(ctx, q)));
     count_launch(ctx);
@@ -1235,7 +1312,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
         int r;
         if (ep && !ep->staged)
           for (PullJob& job : ep->pulls)
-            if (ctx->dev[job.dst].gpu == gi && (r = issue_pull(ctx, job, k, overlap_kernel, halo_kernel))) return r;
+            if (ctx->dev[job.dst].gpu == gi && (r = issue_pull(ctx, t, job, k, overlap_kernel, halo_kernel, scalars))) return r;
         for (int q = 0; q < ctx->P; q++)
           if (ctx->dev[q].local && ctx->dev[q].gpu == gi &&
               (r = issue_kernel(ctx, t, k, q, kernel, scalars, host_in, host_out)))
@@ -1246,7 +1323,7 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     } else {
       if (ep && !ep->staged)
         for (PullJob& job : ep->pulls)
-          if ((rc = issue_pull(ctx, job, k, overlap_kernel, halo_kernel))) return rc;
+          if ((rc = issue_pull(ctx, t, job, k, overlap_kernel, halo_kernel, scalars))) return rc;
       for (int q = 0; q < ctx->P; q++)
         if (ctx->dev[q].local && (rc = issue_kernel(ctx, t, k, q, kernel, scalars, host_in, host_out))) return rc;
     }
@@ -1289,6 +1366,8 @@ static hda_ctx_t* new_ctx(int P) {
   ctx->pulled_on_comm.assign(P, 0);
   ctx->cur_pull.assign(P, nullptr);
   ctx->halo_job.assign(P, nullptr);
+  ctx->split_mode.assign(P, 0);
+  ctx->war_done.assign(P, 0);
   // HDA_TIMEOUT_MS: bound on every cross-device wait (default 60 s); a short value
   // turns a protocol deadlock into a prompt HDA_ETIMEOUT when debugging
   if (int ms = env_int("HDA_TIMEOUT_MS", 0)) ctx->timeout_ns = 1000000LL * ms;
@@ -1518,6 +1597,8 @@ static int create_common(hda_ctx_t* ctx, int32_t dtype, int32_t ndim, const int6
   a.imported = !ctx->spmd || ctx->P == 1 || ctx->plan_only;
   ctx->arr.push_back(a);
   ctx->pend.emplace_back(ctx->P, std::vector<unsigned long long>(ctx->P, 0));
+  ctx->rread.emplace_back(ctx->P);
+  ctx->rread_over.emplace_back(ctx->P, 0);
   *id_out = id;
   return HDA_OK;
 }
