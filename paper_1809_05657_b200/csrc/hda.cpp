@@ -1293,11 +1293,12 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     DevGuard g(true);
     const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
                                 kernel == KN_SCALE || kernel == KN_COPY;
-    // HDA_HALO_MODE: 1 one fused launch (pull blocks + interior + gated boundary strips);
-    // 0 comm-stream pull + interior launch + boundary launch; -1 (default) fused for the
-    // 5-point Jacobi, three launches for the 9-point stencil (measured on 4 B200s,
-    // profiles/r01/README.md: Jacobi 1220 vs 1179 GPoints/s, 9-point 953 vs 1171).
-    static const int halo_mode = env_int("HDA_HALO_MODE", -1);
+    // HDA_HALO_MODE: 0 (default) pull + boundary part on the comm stream, interior on
+    // the main stream (per-box WAR, HDA_COMM_BOUNDARY); 1 one fused launch (pull blocks +
+    // interior + gated boundary strips); -1 fused for the 5-point Jacobi only.  Measured
+    // on 4 B200s (profiles/r01/comm_boundary/): Jacobi N=4 1297 vs 1272 fused, N=2 724 vs
+    // 712; 9-point N=4 1232 (fused: 1045).
+    static const int halo_mode = env_int("HDA_HALO_MODE", 0);
     const bool halo_kernel = (halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9)) ||
                              (halo_mode == -1 && kernel == KN_JACOBI5);
     ExecPlan scratch;
