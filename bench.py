@@ -669,14 +669,20 @@ def main():
         except Exception:
             pass
 
-    # N=1 stencil steps are exactly one kernel launch: take the roofline from the timed
-    # region itself (CUDA events on the kernel's stream), not from the bracketing pass
-    if ws == 1 and isinstance(wl, Stencil) and launches == args.steps:
+    # Stencils: take the roofline from the timed region itself (CUDA events on the
+    # kernel's stream, max over ranks).  At N=1 a step is exactly one launch; at N>1 the
+    # dominant (interior) launch runs concurrently with the pull and the boundary part,
+    # so the per-GPU step time is its duration with the exchange included (conservative);
+    # the event-bracketed pass, which serialises those parts, is kept for reference.
+    if isinstance(wl, Stencil) and (ws > 1 or launches == args.steps):
         roof["avg_launch_ms_bracketed"] = roof["avg_launch_ms"]
         roof["avg_launch_ms"] = ms / args.steps
         roof["achieved"] = wl.alg_per_launch / (roof["avg_launch_ms"] * 1e-3) / 1e9
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["timing"] = "timed region (one launch per step)"
+        roof["timing"] = ("timed region (one launch per step)" if ws == 1 else
+                          "timed region (per-GPU step incl. the overlapped exchange)")
+        if ws > 1:
+            roof["achieved_min_over_ranks"] = roof["achieved"]  # ms is already the max over ranks
     if args.trace:
         barrier()
         h.set_trace(True)
