@@ -1293,14 +1293,24 @@ static int call(hda_ctx_t* ctx, int32_t kernel, hda_part_t part, const AccessIn*
     DevGuard g(true);
     const bool overlap_kernel = kernel == KN_JACOBI5 || kernel == KN_STENCIL9 || kernel == KN_STENCIL7_3D ||
                                 kernel == KN_SCALE || kernel == KN_COPY;
-    // HDA_HALO_MODE: 0 (default) pull + boundary part on the comm stream, interior on
-    // the main stream (per-box WAR, HDA_COMM_BOUNDARY); 1 one fused launch (pull blocks +
-    // interior + gated boundary strips); -1 fused for the 5-point Jacobi only.  Measured
-    // on 4 B200s (profiles/r01/comm_boundary/): Jacobi N=4 1297 vs 1272 fused, N=2 724 vs
-    // 712; 9-point N=4 1232 (fused: 1045).
-    static const int halo_mode = env_int("HDA_HALO_MODE", 0);
+    // HDA_HALO_MODE: 0 split streams — pull + boundary part on the comm stream, interior
+    // on the main stream (per-box WAR, HDA_COMM_BOUNDARY); 1 one fused launch (pull
+    // blocks + interior + gated boundary strips); -1 fused for the 5-point Jacobi only;
+    // -2 (default) split streams, except the fused launch for a 5-point share under
+    // 200 MB of traffic per step, where the split shape's host issue (27 vs 14 us per
+    // step at N=4, measured) would approach the device step.  Measured on 4 B200s
+    // (profiles/r01/comm_boundary/): Jacobi N=4 (268 MB shares) 1297 split vs 1272 fused,
+    // N=2 724 vs 712; 9-point N=4 1232 split (fused: 1045).
+    static const int halo_mode = env_int("HDA_HALO_MODE", -2);
+    bool small_share = false;
+    if (halo_mode == -2 && kernel == KN_JACOBI5) {
+      const TPart& wp = ctx->tr->part(part);
+      const TArray& a0 = ctx->tr->array(ci.param_array[0]);
+      for (int q = 0; q < ctx->P; q++)
+        if (ctx->dev[q].local && box_volume(wp.box[q]) * 2 * (int64_t)a0.es < 200LL * 1000 * 1000) small_share = true;
+    }
     const bool halo_kernel = (halo_mode == 1 && (kernel == KN_JACOBI5 || kernel == KN_STENCIL9)) ||
-                             (halo_mode == -1 && kernel == KN_JACOBI5);
+                             (halo_mode == -1 && kernel == KN_JACOBI5) || small_share;
     ExecPlan scratch;
     ExecPlan* ep = nullptr;
     if ((rc = exchange_plan(ctx, t, k, scratch, &ep))) return rc;
