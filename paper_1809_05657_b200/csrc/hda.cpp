@@ -1095,6 +1095,61 @@ static IssuePool* issue_pool(hda_ctx_t* ctx) {
   return ctx->pool.get();
 }
 
+// the kernel part of a call whose pull runs on the comm stream (overlap): interior boxes
+// while the pull is in flight, dependent boxes after it (or already on the comm stream)
+static int issue_overlapped(hda_ctx_t* ctx, const Transition* t, int q, int32_t kernel, const double* scalars,
+                            KSync& ks) {
+  int rc;
+  // interior boxes while the pull is in flight, dependent boxes after it
+  const PullJob& job = *ctx->cur_pull[q];
+  Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+  bool joined = false;
+  const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
+  if (ctx->split_mode[q] == 2) {  // boundary already issued on the comm stream
+    ctx->split_mode[q] = 0;
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+    if ((rc = run_kernel(ctx, t, q, scalars, ks, &job.interior))) return rc;
+    mark(ctx, q, 2);
+    if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
+    CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+    ctx->pulled_on_comm[q] = 0;
+    return HDA_OK;
+  }
+  if (ks.nwait > 0) {
+    // The peers' pulls this WAR wait depends on need SM time (their pull kernels)
+    // or stall behind GPU-filling kernels (measured: cross-process 3-D peer copies
+    // on the copy engine); if every CTA of the interior spun here while the peers
+    // did the same, neither GPU would free what the other's pull needs.  Wait in
+    // one CTA, then launch the interior with no waits.
+    KSync w = ks_empty(ctx);
+    std::memcpy(w.wait_ptr, ks.wait_ptr, sizeof w.wait_ptr);
+    std::memcpy(w.wait_val, ks.wait_val, sizeof w.wait_val);
+    w.nwait = ks.nwait;
+    if ((rc = sync_only(ctx, q, w))) return rc;
+    ks.nwait = 0;
+  }
+  if (has_i) {
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+    if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, true, !has_d), &job.interior))) return rc;
+    mark(ctx, q, 2);
+    if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
+  }
+  if (has_d) {
+    CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+    joined = true;
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+    if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, !has_i, true), &job.dependent))) return rc;
+    mark(ctx, q, 3);
+    if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
+  }
+  if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+  ctx->pulled_on_comm[q] = 0;
+  return HDA_OK;
+}
+
 // everything device q issues for call k after its pull: WAR waits, the kernel (or the
 // host copy of a write/read), PROD signals.  Thread-safe against other devices' issue.
 static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long k, int q, int32_t kernel,
@@ -1213,53 +1268,7 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
     mark(ctx, q, 1);
     if ((rc = timed_end(ctx, st, kernel, a, 1))) return rc;
   } else if (kern && ctx->pulled_on_comm[q]) {
-    // interior boxes while the pull is in flight, dependent boxes after it
-    const PullJob& job = *ctx->cur_pull[q];
-    Gpu& g = ctx->gpus[ctx->dev[q].gpu];
-    bool joined = false;
-    const bool has_i = !job.interior.empty(), has_d = !job.dependent.empty();
-    if (ctx->split_mode[q] == 2) {  // boundary already issued on the comm stream
-      ctx->split_mode[q] = 0;
-      cudaEvent_t a;
-      if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-      if ((rc = run_kernel(ctx, t, q, scalars, ks, &job.interior))) return rc;
-      mark(ctx, q, 2);
-      if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
-      CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
-      ctx->pulled_on_comm[q] = 0;
-      goto kernel_done;
-    }
-    if (ks.nwait > 0) {
-      // The peers' pulls this WAR wait depends on need SM time (their pull kernels)
-      // or stall behind GPU-filling kernels (measured: cross-process 3-D peer copies
-      // on the copy engine); if every CTA of the interior spun here while the peers
-      // did the same, neither GPU would free what the other's pull needs.  Wait in
-      // one CTA, then launch the interior with no waits.
-      KSync w = ks_empty(ctx);
-      std::memcpy(w.wait_ptr, ks.wait_ptr, sizeof w.wait_ptr);
-      std::memcpy(w.wait_val, ks.wait_val, sizeof w.wait_val);
-      w.nwait = ks.nwait;
-      if ((rc = sync_only(ctx, q, w))) return rc;
-      ks.nwait = 0;
-    }
-    if (has_i) {
-      cudaEvent_t a;
-      if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-      if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, true, !has_d), &job.interior))) return rc;
-      mark(ctx, q, 2);
-      if ((rc = timed_end(ctx, g.stream, kernel, a, 1))) return rc;
-    }
-    if (has_d) {
-      CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
-      joined = true;
-      cudaEvent_t a;
-      if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
-      if ((rc = run_kernel(ctx, t, q, scalars, ks_part(ctx, ks, !has_i, true), &job.dependent))) return rc;
-      mark(ctx, q, 3);
-      if ((rc = timed_end(ctx, g.stream, kernel, a, has_i ? 0 : 1))) return rc;
-    }
-    if (!joined) CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
-    ctx->pulled_on_comm[q] = 0;
+    if ((rc = issue_overlapped(ctx, t, q, kernel, scalars, ks))) return rc;
   } else if (kern) {
     cudaEvent_t a;
     if ((rc = timed_begin(ctx, stream_of(ctx, q), &a))) return rc;
@@ -1269,7 +1278,6 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
   } else if ((rc = sync_only(ctx, q, ks))) {  // K_NONE definitions
     return rc;
   }
-kernel_done:
   if (split_sig) {
     CK(launch_signal_pdl(post_sig, ks.relaxed, stream_of(ctx, q)));
     count_launch(ctx);
