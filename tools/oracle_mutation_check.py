@@ -20,6 +20,15 @@ MUTS = [
     ("remainder rule", "int64_t st = lo + (int64_t)i * b + (i < r ? i : r);", "int64_t st = lo + (int64_t)i * b;"),
     ("gemm transposed B", "lin(B, kk, j, 0)", "lin(B, j, kk, 0)"),
     ("stencil7 z- twice", "s = s + rdf32(k, X, lin(X, z + 1, y, x));", "s = s + rdf32(k, X, lin(X, z - 1, y, x));"),
+    ("trapezoid rounds half down", "left = ul + floordiv((r - top) * (bl - ul) * 2 + h, 2 * h);",
+     "left = ul + floordiv((r - top) * (bl - ul) * 2 + h - 1, 2 * h);"),
+    ("trapezoid drops the bottom row", "for (int64_t r = top; r <= bottom; r++) {",
+     "for (int64_t r = top; r < bottom; r++) {"),
+    ("reduce PROD sums", "else if (op == ORC_PROD) acc = acc * v;", "else if (op == ORC_PROD) acc = acc + v;"),
+    ("reduce skips coherence", "int rc = orc_read(w, arr, part, NULL); /* coherence, exactly as a read */",
+     "int rc = 0;"),
+    ("absolute defs never commit", "          A[e]->owner[c] = definer[e][c];\n          A[e]->valid[c] = 1ULL << definer[e][c];",
+     "          (void)0;"),
 ]
 
 
