@@ -306,3 +306,53 @@ class Program:
         empty = [[] for _ in range(self.h.P)]
         acc = [(val[n], slots.get(n, {}).get("use", empty), slots.get(n, {}).get("def", empty)) for n in arrays]
         return self.h.apply_abs(kid, part, acc, sc)
+
+
+def _cname(s: str) -> str:
+    return re.sub(r"\W", "_", s)
+
+
+def emit_c(fm: dict) -> str:
+    """Task (3) of the paper's frontend: the file-M table as C for host
+    programs written against include/hdarray.h — per offset-annotated kernel an
+    access-list builder in the kernel's array-parameter order, per `partition`
+    clause a function that creates the manual partition (hda_partition_manual)."""
+    out = ["/* generated by paper_1809_05657_b200.frontend from #pragma hdarray clauses */",
+           "#include <stdint.h>", '#include "hdarray.h"', ""]
+    for name, k in fm["kernels"].items():
+        arrays = [p["name"] for p in k["params"] if p["array"]]
+        accs = [k["access"].get(a, {"use": [], "def": [], "use_abs": False, "def_abs": False}) for a in arrays]
+        if any(a["use_abs"] or a["def_abs"] for a in accs):
+            out.append(f"/* kernel {name}: absolute sections (use@/def@) — build hda_abs_access_t at run time */")
+            out.append("")
+            continue
+        cn = _cname(name)
+        for a, acc in zip(arrays, accs):
+            for kind in ("use", "def"):
+                flat = [("HDA_STAR" if v == "*" else str(int(v))) for t in acc[kind] for v in t]
+                body = ", ".join(flat) if flat else "0"
+                out.append(f"static const int32_t hdam_{cn}_{_cname(a)}_{kind}[] = {{{body}}};")
+        out.append(f"/* kernel {name}: arrays in parameter order: {', '.join(arrays)} */")
+        out.append(f"static inline int32_t hdam_{cn}_n_arrays(void) {{ return {len(arrays)}; }}")
+        out.append(f"static inline void hdam_{cn}_access(hda_access_t* acc, const hda_array_t* arrays) {{")
+        for i, (a, acc) in enumerate(zip(arrays, accs)):
+            ca = _cname(a)
+            out.append(f"  acc[{i}].array = arrays[{i}];")
+            out.append(f"  acc[{i}].n_use = {len(acc['use'])};")
+            out.append(f"  acc[{i}].use = hdam_{cn}_{ca}_use;")
+            out.append(f"  acc[{i}].n_def = {len(acc['def'])};")
+            out.append(f"  acc[{i}].def = hdam_{cn}_{ca}_def;")
+        out.append("}")
+        out.append("")
+    for pid, p in fm["partitions"].items():
+        nd, P = len(p["domain"]), len(p["lb"])
+        dom = ", ".join(str(v) for v in p["domain"])
+        lbs = ", ".join(str(v) for row in p["lb"] for v in row)
+        ubs = ", ".join(str(v) for row in p["ub"] for v in row)
+        out.append(f"/* partition {pid}: {P} devices, (start, length) pairs read as R2 */")
+        out.append(f"static inline int hdam_partition_{_cname(pid)}(hda_ctx_t* ctx, hda_part_t* out) {{")
+        out.append(f"  static const int64_t dom[] = {{{dom}}}, lbs[] = {{{lbs}}}, ubs[] = {{{ubs}}};")
+        out.append(f"  return hda_partition_manual(ctx, {nd}, dom, lbs, ubs, out);")
+        out.append("}")
+        out.append("")
+    return "\n".join(out)

@@ -171,3 +171,52 @@ def test_mixed_offset_and_absolute_rejected():
     with pytest.raises(ValueError, match="mixing"):
         prog.apply_kernel("m", p, Y, X)
     h.close()
+
+
+def test_emitted_c_drives_the_c_abi(tmp_path):
+    """The frontend's C output (P:L372 task 3) compiles against include/hdarray.h and,
+    linked with libhdarray.so in a plan-only context, plans the expected halo: the
+    second Jacobi call moves row 7 (device 0 -> 1) and row 8 (1 -> 0), columns [1,15)."""
+    import os
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("needs gcc")
+    src = JACOBI_CU + r"""
+#pragma hdarray partition(work, (16,16), dev:0, (1,7),(1,14), dev:1, (8,7),(1,14))
+"""
+    gen = F.emit_c(F.parse(src))
+    (tmp_path / "hdam.h").write_text(gen)
+    (tmp_path / "main.c").write_text(r'''
+#include <stdio.h>
+#include "hdam.h"
+int main(void) {
+  hda_ctx_t* ctx; hda_array_t A, B; hda_part_t w;
+  const int64_t shape[2] = {16, 16};
+  if (hda_init(&ctx, 0, NULL, 2)) return 1;
+  if (hda_create(ctx, HDA_F64, 2, shape, NULL, &A) || hda_create(ctx, HDA_F64, 2, shape, NULL, &B)) return 2;
+  if (hdam_partition_work(ctx, &w)) return 3;
+  hda_access_t acc[2];
+  hda_array_t ab[2] = {A, B}, ba[2] = {B, A};
+  hdam_jacobi_step_access(acc, ab);
+  if (hda_apply(ctx, HDA_K_JACOBI5, w, acc, hdam_jacobi_step_n_arrays(), NULL, 0)) return 4;
+  hdam_jacobi_step_access(acc, ba);
+  if (hda_apply(ctx, HDA_K_JACOBI5, w, acc, 2, NULL, 0)) return 5;
+  hda_msg_t m[8]; int32_t n = 0;
+  if (hda_last_plan(ctx, m, 8, &n)) return 6;
+  for (int i = 0; i < n; i++)
+    printf("%d %d %d %lld %lld %lld %lld\n", m[i].array, m[i].src, m[i].dst, (long long)m[i].lb[0],
+           (long long)m[i].ub[0], (long long)m[i].lb[1], (long long)m[i].ub[1]);
+  return hda_finalize(ctx);
+}
+''')
+    libdir = os.path.dirname(H.lib()._name)
+    inc = os.path.join(os.path.dirname(libdir), "include")
+    exe = str(tmp_path / "main")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", inc, "-I", str(tmp_path),
+                    str(tmp_path / "main.c"), "-o", exe, "-L", libdir, "-lhdarray",
+                    "-Wl,-rpath," + libdir], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, (r.returncode, r.stderr)
+    rows = sorted(tuple(int(v) for v in line.split()) for line in r.stdout.split("\n") if line.strip())
+    assert rows == [(0, 0, 1, 7, 8, 1, 15), (0, 1, 0, 8, 9, 1, 15)]
