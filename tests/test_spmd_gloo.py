@@ -59,7 +59,7 @@ def _worker(rank, world, port, q):
     del local
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_spmd_replicated_tracker_gloo(world):
     import paper_1809_05657_b200 as H
     H.lib()
