@@ -223,6 +223,20 @@ static int nparams(int32_t kernel) {
   return -2;
 }
 
+// per-kernel minimum scalar count: checked on EVERY call, cache hit or not (the spec
+// key does not hold the scalar values, so a cached spec says nothing about them)
+static int check_scalars(int32_t kernel, int32_t n_scalars, std::string& err) {
+  if ((kernel == KN_SCALE || kernel == KN_STAMP) && n_scalars < 1) {
+    err = "kernel needs scalars[0]";
+    return HDA_EINVAL;
+  }
+  if (kernel == KN_GEMM && n_scalars < 2) {
+    err = "GEMM needs scalars {alpha, beta}";
+    return HDA_EINVAL;
+  }
+  return HDA_OK;
+}
+
 int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* acc, int32_t n_acc,
                                   const double* scalars, int32_t n_scalars, CallInfo& ci,
                                   std::string& err) const {
@@ -274,10 +288,7 @@ int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* 
         return HDA_EINVAL;
       }
   }
-  if ((kernel == KN_SCALE || kernel == KN_STAMP) && n_scalars < 1) {
-    err = "kernel needs scalars[0]";
-    return HDA_EINVAL;
-  }
+  if (int rc = check_scalars(kernel, n_scalars, err)) return rc;
   if (kernel == KN_STAMP) {
     if (n_acc < 1) {
       err = "STAMP needs at least the stamped array";
@@ -292,10 +303,6 @@ int Tracker::validate_and_compose(int32_t kernel, int32_t part, const AccessIn* 
         return HDA_EINVAL;
       }
     }
-  }
-  if (kernel == KN_GEMM && n_scalars < 2) {
-    err = "GEMM needs scalars {alpha, beta}";
-    return HDA_EINVAL;
   }
   const int32_t zero[3] = {0, 0, 0};
   int64_t halo = 0;
@@ -581,6 +588,7 @@ void Tracker::compute(const CallInfo& ci, Transition& t) {
 int Tracker::plan(int32_t kernel, int32_t part, const AccessIn* acc, int32_t n_acc,
                   const double* scalars, int32_t n_scalars, bool use_cache,
                   const Transition** out, bool* hit, std::string& err) {
+  if (int rc = check_scalars(kernel, n_scalars, err)) return rc;
   // exact spec key
   std::vector<int64_t>& key = key_;
   key.clear();

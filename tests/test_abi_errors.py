@@ -112,3 +112,25 @@ def test_rejected_calls_leave_no_trace():
     np.testing.assert_array_equal(h.owner_map(A), w.owner_map(Aw))
     np.testing.assert_array_equal(h.owner_map(B), w.owner_map(Bw))
     h.close()
+
+
+def test_scalar_count_checked_on_cache_hits(h):
+    """The per-kernel scalar minimum holds on every call, not only the first: a valid
+    SCALE / GEMM call caches its spec, and the same call with too few scalars is still
+    EINVAL (the GPU path would otherwise read scalars[0] / scalars[1] past the array)."""
+    X = h.create(H.F64, (8, 8))
+    p = h.partition(H.ROW, (8, 8))
+    acc = [(X, [(0, 0)], [(0, 0)])]
+    h.apply(H.K_SCALE, p, acc, (2.0,))
+    for bad in ((), ):
+        with pytest.raises(H.HDAError) as e:
+            h.apply(H.K_SCALE, p, acc, bad)
+        assert e.value.code == H.EINVAL and "scalars" in str(e.value)
+    A, B, C = (h.create(H.BF16, (8, 8)) for _ in range(3))
+    g = [(C, [], [(0, 0)]), (A, [(0, H.STAR)], []), (B, [(H.STAR, 0)], [])]
+    h.apply(H.K_GEMM, p, g, (1.0, 0.0))
+    for bad in ((), (1.0,)):
+        with pytest.raises(H.HDAError) as e:
+            h.apply(H.K_GEMM, p, g, bad)
+        assert e.value.code == H.EINVAL
+    h.apply(H.K_SCALE, p, acc, (2.0,))  # the context is still usable
