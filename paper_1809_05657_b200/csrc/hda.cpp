@@ -52,7 +52,8 @@ constexpr int SW_PULLDONE = 194;  // local: epoch of the last completed overlapp
 constexpr int SW_RED = 256, SW_REDSIG = 320;  // reduce partials [P] and their epochs [P]
 constexpr int SW_DEBUG = 195;                  // measurement hooks only
 constexpr int SW_SCRATCH = 384;               // kReduceBlocks partials
-constexpr int SW_WORDS = SW_SCRATCH + kReduceBlocks;
+constexpr int SW_RED_B = SW_SCRATCH + kReduceBlocks;  // second bank of reduce partials [P]
+constexpr int SW_WORDS = SW_RED_B + 64;
 constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
 constexpr int64_t kCeBytes = 1 << 20;         // AUTO: messages >= 1 MiB go to the copy engine
 
@@ -212,6 +213,10 @@ struct hda_ctx {
   std::vector<std::vector<std::vector<Box>>> rread;
   std::vector<std::vector<char>> rread_over;
   std::vector<int> split_mode;  // per device: 2 = this call's boundary part ran on the comm stream
+  // [P] WAR waits of this call's pull into device q's replica: (ACK word, epoch) of the
+  // peers that pulled those cells from q earlier and may still be reading them
+  std::vector<std::vector<std::pair<unsigned long long*, unsigned long long>>> pull_war;
+  unsigned long long n_reduce = 0;  // reduce calls so far (identical on every SPMD rank)
   std::vector<char> war_done;   // per device: WAR waits already issued for this call
   std::vector<std::vector<std::pair<int, unsigned long long>>> stage_pend;  // [src]
   std::vector<char*> send_stage, recv_stage;
@@ -403,8 +408,8 @@ static int env_int(const char* name, int dflt) {
 }
 
 static KSync ks_empty(hda_ctx_t* ctx) {
-  // signals are relaxed system-scope stores issued after a gpu-scope fence (sync.cuh);
-  // HDA_SIG_RELEASE=1 switches to st.release.sys (measured ~4 us slower per launch)
+  // signals: one system-scope fence, then relaxed system-scope stores — a release at
+  // system scope (sync.cuh); HDA_SIG_RELEASE=1 uses st.release.sys for every flag
   static const int relaxed = env_int("HDA_SIG_RELEASE", 0) ? 0 : 1;
   KSync k;
   k.relaxed = relaxed;
@@ -418,10 +423,13 @@ static KSync ks_empty(hda_ctx_t* ctx) {
   return k;
 }
 // test hook: every pull (the reader side of an exchange) sleeps this long after its
-// RAW waits, so a missing WAR wait on the writer shows up as a parity failure
-static long long pull_delay_ns() {
+// RAW waits, so a missing WAR wait on the writer shows up as a parity failure;
+// HDA_DEBUG_PULL_DELAY_DEV=r delays only reader device r's pulls (an asymmetric slow
+// reader: the WAR windows that only open while OTHER devices run ahead)
+static long long pull_delay_ns(int q) {
   static const long long v = 1000LL * env_int("HDA_DEBUG_PULL_DELAY_US", 0);
-  return v;
+  static const int only = env_int("HDA_DEBUG_PULL_DELAY_DEV", -1);
+  return only < 0 || only == q ? v : 0;
 }
 static void ks_wait(KSync& k, unsigned long long* p, unsigned long long v) {
   if (v == 0) return;
@@ -458,10 +466,11 @@ static int sync_all(hda_ctx_t* ctx) {
 
 // ====================================================================== exec plans
 
+// grows device d's staging buffer; the caller has synchronised EVERY GPU first (a
+// peer's in-flight copy may still read the old send buffer)
 static int ensure_stage(hda_ctx_t* ctx, std::vector<char*>& v, std::vector<size_t>& cap, int d, size_t need) {
   if (cap[d] >= need) return HDA_OK;
   CK(cudaSetDevice(ordinal_of(ctx, d)));
-  CK(cudaStreamSynchronize(stream_of(ctx, d)));
   if (v[d]) CK(cudaFree(v[d]));
   size_t n = std::max(need, (size_t)1 << 20);
   CK(cudaMalloc((void**)&v[d], n));
@@ -571,12 +580,8 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
     src_off[i] = used[m.src];
     used[m.src] += ((size_t)box_volume(m.box) * a.es + 255) & ~(size_t)255;
   }
-  for (int p = 0; p < P; p++) {
-    if (!ctx->dev[p].local || used[p] == 0) continue;
-    int rc = ensure_stage(ctx, ctx->send_stage, ctx->send_cap, p, used[p]);
-    if (rc) return rc;
-  }
-  // packs
+  // packs (staging pointers are bound at issue, issue_staged: a cached plan must not
+  // hold a buffer that a later, larger plan reallocates)
   for (int p = 0; p < P; p++) {
     if (!ctx->dev[p].local || used[p] == 0) continue;
     PackJob job;
@@ -591,7 +596,7 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
       front_shape(a.ndim, a.shape, S);
       RunDesc d = rect_desc(S, front_box(a.ndim, m.box), a.es);
       d.src = ctx->arr[m.array].ptr[p];
-      d.dst = ctx->send_stage[p];
+      d.dst = nullptr;  // send_stage[p], bound at issue
       d.dst_off = (int64_t)src_off[i];
       d.dst_p1 = d.run_bytes;
       d.dst_p0 = d.run_bytes * d.n1;
@@ -633,9 +638,7 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
     }
     if (descs.empty()) continue;
     job.bytes = off;
-    int rc = ensure_stage(ctx, ctx->recv_stage, ctx->recv_cap, q, off);
-    if (rc) return rc;
-    for (RunDesc& d : descs) d.src = ctx->recv_stage[q];
+    for (RunDesc& d : descs) d.src = nullptr;  // recv_stage[q], bound at issue
     batch_descs(descs, job.unpack);
     ep.recvs.push_back(std::move(job));
   }
@@ -664,11 +667,52 @@ static int timed_end(hda_ctx_t* ctx, cudaStream_t st, int kind, cudaEvent_t a, i
   return HDA_OK;
 }
 
+// WAR on the READER side: a pull overwrites cells of its reader q's own replica, so
+// every peer r that pulled cells of that array from q since q last wrote it (pend,
+// rread) and may still be reading them — r's stream can run far behind q's — must have
+// acknowledged before the pull writes.  Three devices are enough: q writes c, r pulls
+// c from q, p redefines c (waiting on no one: r read q's replica, not p's), then q
+// pulls c back from p.  Filtered per box: a pull whose boxes miss every box peers read
+// from q's replica waits on nothing (the steady state of every halo loop, where q's
+// own definition of the array cleared both records first).  Computed from the records
+// BEFORE this call's reads are added: within one call q pulls only cells it does not
+// own and peers pull only cells it owns, and waiting on this call's own ACKs would
+// deadlock a symmetric halo exchange.
+static void pull_war_waits(hda_ctx_t* ctx, const Transition* t) {
+  static const int no_war = env_int("HDA_DEBUG_NO_WAR", 0);
+  for (auto& v : ctx->pull_war) v.clear();
+  if (no_war) return;
+  for (const Msg& m : t->msgs) {
+    const int q = m.dst;
+    if (!ctx->dev[q].local) continue;
+    const auto& row = ctx->pend[m.array][q];
+    bool any = false;
+    for (int r = 0; r < ctx->P; r++) any |= row[r] && !same_stream(ctx, q, r);
+    if (!any) continue;
+    bool hit = ctx->rread_over[m.array][q] != 0;
+    for (const Box& b : ctx->rread[m.array][q]) hit = hit || !box_empty(box_and(b, m.box));
+    if (!hit) continue;
+    auto& w = ctx->pull_war[q];
+    for (int r = 0; r < ctx->P; r++) {
+      if (!row[r] || same_stream(ctx, q, r)) continue;
+      unsigned long long* p = ctx->dev[q].sync + SW_ACK + r;
+      bool merged = false;
+      for (auto& e : w)
+        if (e.first == p) {
+          e.second = std::max(e.second, row[r]);
+          merged = true;
+        }
+      if (!merged) w.emplace_back(p, row[r]);
+    }
+  }
+}
+
 // exec plan of call t (cached per transition) and the WAR bookkeeping of its reads
 // (`scratch` holds the plan when the cache is off; it must outlive the issue)
 static int exchange_plan(hda_ctx_t* ctx, const Transition* t, unsigned long long k, ExecPlan& scratch,
                          ExecPlan** out) {
   *out = nullptr;
+  pull_war_waits(ctx, t);
   if (t->msgs.empty()) return HDA_OK;
   ExecPlan* ep;
   if (ctx->cache_on) {
@@ -716,7 +760,8 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
   Gpu& g = ctx->gpus[ctx->dev[q].gpu];
   // 2-D stencil with a cross-GPU halo: the pull runs inside the stencil launch
   if (ctx->overlap && halo_kernel && job.cross && job.split && job.ce.empty() && job.batches.size() == 1 &&
-      job.srcs.size() <= 8 && job.interior.size() + job.dependent.size() <= 8) {
+      job.srcs.size() <= 8 && job.srcs.size() + ctx->pull_war[q].size() <= 16 &&
+      job.interior.size() + job.dependent.size() <= 8) {
     ctx->halo_job[q] = &job;
     return HDA_OK;
   }
@@ -754,6 +799,7 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
       ks_sig(post, ctx->dev[p].sync + SW_ACK + q);
     }
   for (int i = 0; i < war.nwait; i++) ks_wait(pre, war.wait_ptr[i], war.wait_val[i]);
+  for (const auto& e : ctx->pull_war[q]) ks_wait(pre, e.first, e.second);
   int rc;
   cudaEvent_t a = nullptr;
   const size_t nb = job.batches.size();
@@ -763,7 +809,7 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
     std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
     std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
     w.nwait = pre.nwait;
-    w.delay_ns = pull_delay_ns();
+    w.delay_ns = pull_delay_ns(q);
     RunBatch empty;
     std::memset(&empty, 0, sizeof empty);
     if (w.nwait || w.delay_ns) {
@@ -784,7 +830,7 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
       std::memcpy(ks.wait_ptr, pre.wait_ptr, sizeof ks.wait_ptr);
       std::memcpy(ks.wait_val, pre.wait_val, sizeof ks.wait_val);
       ks.nwait = pre.nwait;
-      ks.delay_ns = pull_delay_ns();
+      ks.delay_ns = pull_delay_ns(q);
     }
     if (i + 1 == nb) {
       std::memcpy(ks.sig_ptr, post.sig_ptr, sizeof ks.sig_ptr);
@@ -809,8 +855,30 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
   return HDA_OK;
 }
 
+static RunBatch bind_stage(const RunBatch& b, char* dst, const char* src) {
+  RunBatch o = b;
+  for (int i = 0; i < o.n; i++) {
+    if (dst) o.d[i].dst = dst;
+    if (src) o.d[i].src = src;
+  }
+  return o;
+}
+
 // STAGED transport (single process, serial issue)
 static int issue_staged(hda_ctx_t* ctx, ExecPlan* ep, unsigned long long k) {
+  // size the staging buffers for this plan; growing one first drains every GPU, so no
+  // pack, peer copy or unpack of an earlier call still uses the buffer being freed
+  bool grow = false;
+  for (const PackJob& job : ep->packs) grow |= ctx->send_cap[job.src] < job.bytes;
+  for (const RecvJob& job : ep->recvs) grow |= ctx->recv_cap[job.dst] < job.bytes;
+  if (grow) {
+    int rc = sync_all(ctx);
+    if (rc) return rc;
+    for (const PackJob& job : ep->packs)
+      if ((rc = ensure_stage(ctx, ctx->send_stage, ctx->send_cap, job.src, job.bytes))) return rc;
+    for (const RecvJob& job : ep->recvs)
+      if ((rc = ensure_stage(ctx, ctx->recv_stage, ctx->recv_cap, job.dst, job.bytes))) return rc;
+  }
   for (PackJob& job : ep->packs) {
     const int p = job.src;
     CK(cudaSetDevice(ordinal_of(ctx, p)));
@@ -824,7 +892,7 @@ static int issue_staged(hda_ctx_t* ctx, ExecPlan* ep, unsigned long long k) {
     cudaEvent_t a;
     if ((rc = timed_begin(ctx, stream_of(ctx, p), &a))) return rc;
     for (const RunBatch& b : job.batches) {
-      CK(launch_copy_runs(b, ks_empty(ctx), stream_of(ctx, p)));
+      CK(launch_copy_runs(bind_stage(b, ctx->send_stage[p], nullptr), ks_empty(ctx), stream_of(ctx, p)));
       count_launch(ctx);
     }
     if ((rc = timed_end(ctx, stream_of(ctx, p), -100, a))) return rc;
@@ -848,6 +916,7 @@ static int issue_staged(hda_ctx_t* ctx, ExecPlan* ep, unsigned long long k) {
         wl_add(wl, ctx->dev[q].sync + SW_PACK + p, k);
         sl.ptr[sl.n++] = ctx->dev[p].sync + SW_ACK + q;
       }
+    for (const auto& e : ctx->pull_war[q]) wl_add(wl, e.first, e.second);
     int rc = launch_waits(ctx, q, wl);
     if (rc) return rc;
     cudaEvent_t a;
@@ -856,7 +925,7 @@ static int issue_staged(hda_ctx_t* ctx, ExecPlan* ep, unsigned long long k) {
       CK(cudaMemcpyAsync(ctx->recv_stage[q] + s.dst_off, ctx->send_stage[s.src] + s.src_off, s.bytes,
                          cudaMemcpyDeviceToDevice, stream_of(ctx, q)));
     for (const RunBatch& b : job.unpack) {
-      CK(launch_copy_runs(b, ks_empty(ctx), stream_of(ctx, q)));
+      CK(launch_copy_runs(bind_stage(b, nullptr, ctx->recv_stage[q]), ks_empty(ctx), stream_of(ctx, q)));
       count_launch(ctx);
     }
     if ((rc = timed_end(ctx, stream_of(ctx, q), -100, a))) return rc;
@@ -1254,10 +1323,14 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
         }
         hp.ack_ptr[hp.nack++] = ctx->dev[p].sync + SW_ACK + q;
       }
+    for (const auto& e : ctx->pull_war[q]) {
+      hp.wait_ptr[hp.nwait] = e.first;
+      hp.wait_val[hp.nwait++] = e.second;
+    }
     hp.ctr = (unsigned int*)(ctx->dev[q].sync + SW_CTR_PULL);
     hp.done_word = ctx->dev[q].sync + SW_PULLDONE;
     hp.epoch = k;
-    hp.delay_ns = pull_delay_ns();
+    hp.delay_ns = pull_delay_ns(q);
     auto P_ = [&](int param) { return ctx->arr[ci.param_array[param]].ptr[q]; };
     cudaStream_t st = stream_of(ctx, q);
     cudaEvent_t a;
@@ -1386,6 +1459,7 @@ static hda_ctx_t* new_ctx(int P) {
   ctx->cur_pull.assign(P, nullptr);
   ctx->halo_job.assign(P, nullptr);
   ctx->split_mode.assign(P, 0);
+  ctx->pull_war.assign(P, {});
   ctx->war_done.assign(P, 0);
   // HDA_TIMEOUT_MS: bound on every cross-device wait (default 60 s); a short value
   // turns a protocol deadlock into a prompt HDA_ETIMEOUT when debugging
@@ -1826,6 +1900,12 @@ int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, dou
   const TPart& pt = ctx->tr->part(part);
   const bool is_int = a.dtype == DT_I32 || a.dtype == DT_I64;
   const unsigned long long k = ++ctx->epoch;
+  // SPMD: peers write their partials into this rank's slots.  Alternating two banks
+  // keeps a fast rank's partial of the NEXT reduce out of the slots this rank's host
+  // may still be reading: to start reduce n+2 (same bank as n) a rank must have seen
+  // every peer's share of reduce n+1, which each peer issues only after its host
+  // finished reading reduce n.
+  const int red = (ctx->n_reduce++ & 1) ? SW_RED_B : SW_RED;
   DevGuard g(true);
   int64_t S[3];
   front_shape(a.ndim, a.shape, S);
@@ -1834,7 +1914,7 @@ int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, dou
     CK(cudaSetDevice(ordinal_of(ctx, q)));
     unsigned long long* sw = ctx->dev[q].sync;
     const Box fb = front_box(a.ndim, pt.box[q]);
-    CK(launch_reduce(a.dtype, ctx->arr[arr].ptr[q], S, fb.lb, fb.ub, op, sw + SW_SCRATCH, sw + SW_RED + q,
+    CK(launch_reduce(a.dtype, ctx->arr[arr].ptr[q], S, fb.lb, fb.ub, op, sw + SW_SCRATCH, sw + red + q,
                      stream_of(ctx, q)));
     count_launch(ctx, 2);
     if (ctx->spmd && ctx->P > 1) {  // publish this rank's partial to every peer
@@ -1843,10 +1923,10 @@ int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, dou
       flags.val = k;
       for (int r = 0; r < ctx->P; r++) {
         if (r == q) continue;
-        slots.ptr[slots.n++] = ctx->dev[r].sync + SW_RED + q;
+        slots.ptr[slots.n++] = ctx->dev[r].sync + red + q;
         flags.ptr[flags.n++] = ctx->dev[r].sync + SW_REDSIG + q;
       }
-      CK(launch_share(sw + SW_RED + q, slots, flags, stream_of(ctx, q)));
+      CK(launch_share(sw + red + q, slots, flags, stream_of(ctx, q)));
       KSync w = ks_empty(ctx);
       for (int r = 0; r < ctx->P; r++)
         if (r != q) ks_wait(w, sw + SW_REDSIG + r, k);
@@ -1855,6 +1935,10 @@ int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, dou
     }
   }
   if ((rc = sync_all(ctx))) return rc;
+  // test hook: a host that reads its partials late (the window in which a fast peer's
+  // next reduce could overwrite them without the bank alternation above)
+  static const int read_delay_us = env_int("HDA_DEBUG_REDUCE_READ_DELAY_US", 0);
+  if (read_delay_us) std::this_thread::sleep_for(std::chrono::microseconds(read_delay_us));
   // combine the P partials in device order (identical on every rank)
   double acc = op == HDA_SUM ? 0.0 : op == HDA_PROD ? 1.0 : op == HDA_MAX ? -HUGE_VAL : HUGE_VAL;
   long long iacc = op == HDA_PROD ? 1 : op == HDA_MAX ? LLONG_MIN : op == HDA_MIN ? LLONG_MAX : 0;
@@ -1862,7 +1946,7 @@ int hda_reduce(hda_ctx_t* ctx, hda_array_t arr, hda_part_t part, int32_t op, dou
     int src = ctx->spmd ? ctx->rank : p;  // where p's partial lives in this process
     unsigned long long bits = 0;
     CK(cudaSetDevice(ordinal_of(ctx, src)));
-    CK(cudaMemcpy(&bits, ctx->dev[src].sync + SW_RED + p, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&bits, ctx->dev[src].sync + red + p, 8, cudaMemcpyDeviceToHost));
     if (is_int) {
       long long v;
       std::memcpy(&v, &bits, 8);

@@ -285,10 +285,13 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cud
 // the kernel before it on the stream has completed — all of its writes are in this
 // GPU's L2, where peers read them — so no CTA of the big kernel pays a fence + counter
 // at its end (measured: 1.5 us/step for a one-wave share, 8 us for 8192^2 N=1 tiles).
+// griddepcontrol.wait orders the previous kernel's writes before this thread; the
+// system-scope fence then makes the relaxed system-scope flag stores a release at
+// system scope (fence cumulativity), which a peer's ld.acquire.sys synchronises with.
 __global__ void signal_pdl_kernel(const __grid_constant__ SignalList l, int relaxed) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __threadfence();
+  if (relaxed) __threadfence_system();
   const int i = threadIdx.x;
   if (i < l.n) {
     if (relaxed)
@@ -473,8 +476,8 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
 // The pull blocks are dispatched first and wait on nothing inside the kernel, so the
 // dependent blocks' in-kernel wait always makes progress.
 struct PullPart {
-  unsigned long long* wait_ptr[8];
-  unsigned long long wait_val[8];
+  unsigned long long* wait_ptr[16];
+  unsigned long long wait_val[16];
   unsigned long long* ack_ptr[8];
   int32_t nwait, nack, nblocks;
   unsigned int* ctr;
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 0 ? HALO_MINB0 : ST_MINB)
       __threadfence();
       if (atomicAdd(pp.ctr, 1u) == (unsigned)pp.nblocks - 1) {
         *pp.ctr = 0;
-        __threadfence();
+        __threadfence_system();  // release at system scope for the relaxed flag stores
         asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.done_word), "l"(pp.epoch) : "memory");
         for (int i = 0; i < pp.nack; i++)
           asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(pp.ack_ptr[i]), "l"(pp.epoch) : "memory");

@@ -85,8 +85,8 @@ cudaError_t launch_signal_pdl(const SignalList& l, int relaxed, cudaStream_t s);
 // (peer replica -> this replica) in its first blocks, then computes boxes
 // [0, n_interior) immediately and boxes [n_interior, nb) after the pull — one launch.
 struct HaloPull {
-  unsigned long long* wait_ptr[8];  // local PROD words of the sources
-  unsigned long long wait_val[8];
+  unsigned long long* wait_ptr[16];  // local PROD words of the sources, then the pull's WAR ACK words
+  unsigned long long wait_val[16];
   unsigned long long* ack_ptr[8];   // sources' ACK words for this reader
   int32_t nwait, nack;
   unsigned int* ctr;                // local counter

@@ -64,11 +64,11 @@ __device__ __forceinline__ void ks_post(const KSync& s) {
     if (atomicAdd(s.ctr, 1u) == total - 1) {
       *s.ctr = 0;  // stream-ordered reuse by the next kernel of this purpose
       // Every block fenced at gpu scope before the counter, so all of this kernel's
-      // writes to this GPU's memory have reached its L2 — the point peers read this
-      // memory through — and all of its loads (pulls) have returned.  A relaxed
-      // system-scope store of the flag is then enough; st.release.sys costs ~4 us per
-      // signalling launch (measured: N=4 Jacobi 1068 -> 1159 GPoints/s).
-      __threadfence();
+      // writes (and the loads of a pull) happen before this thread's counter update.
+      // A system-scope fence here, then relaxed system-scope stores, is a release at
+      // system scope (fence cumulativity), which the peers' ld.acquire.sys of the flag
+      // synchronises with — one fence for all flags instead of st.release.sys per flag.
+      __threadfence_system();
       if (s.relaxed) {
         for (int i = 0; i < s.nsig; i++)
           asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(s.sig_ptr[i]), "l"(s.sig_val) : "memory");

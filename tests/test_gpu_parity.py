@@ -578,3 +578,39 @@ def test_gemm_cta_pair_ragged(H, cdt, P):
         be.apply(H.K_GEMM, pc, [(C, [(0, 0)], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.0, 2.0])
     assert_replicas(h, w, [C], P)
     h.close()
+
+
+# ------------------------------------------------------------------ WAR races
+def _scenario(name, G, **env):
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ, HDA_TIMEOUT_MS="20000", **env)
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "war_scenarios.py")
+    return subprocess.run([sys.executable, script, name, str(G)], env=e, capture_output=True, text=True,
+                          timeout=600)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_pull_war_three_devices(G):
+    """Reader-side WAR with three devices and an asymmetric slow reader (device 1's
+    pulls sleep 20 ms): a pull into q's replica waits for the ACK of every peer that
+    earlier pulled those cells from q.  Negative control: with the WAR waits switched
+    off (HDA_DEBUG_NO_WAR) the same program breaks parity, so the scenario has teeth."""
+    if ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    slow = dict(HDA_DEBUG_PULL_DELAY_US="20000", HDA_DEBUG_PULL_DELAY_DEV="1")
+    r = _scenario("pull_war", G, **slow)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    neg = _scenario("pull_war", G, HDA_DEBUG_NO_WAR="1", **slow)
+    assert neg.returncode == 1 and "MISMATCH" in neg.stdout, neg.stdout[-3000:] + neg.stderr[-3000:]
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_staged_plan_replay_after_regrow(G):
+    """STAGED: cached small-message plans replayed after a larger plan regrew the
+    staging buffers stay bit-exact (the staging pointers are bound at issue)."""
+    if ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    r = _scenario("staged_regrow", G)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

@@ -105,7 +105,7 @@ def _worker(rank, world, port, q, env1):
         ints = np.arange(np.prod(shape), dtype=np.float64).reshape(shape) % 97
         for be in (h, w):
             be.write(X, full, ints)
-        for op in (H.SUM, H.MAX, H.MIN):
+        for op in (H.SUM, H.MAX, H.MIN, H.SUM, H.MIN, H.MAX):  # back to back, distinct partials
             g, o = h.reduce(X, colp, op), w.reduce(X, colp, op)
             if g != o:
                 bad.append(("reduce", op, g, o))
@@ -140,7 +140,9 @@ def _run(world, env1):
 
 # HDA_DEBUG_PULL_DELAY_US makes rank 1's pulls sleep after their RAW waits: a writer
 # that overwrote cells without waiting for rank 1's ACK would break parity.
-@pytest.mark.parametrize("env1", [{}, {"HDA_DEBUG_PULL_DELAY_US": "300"},
+# HDA_DEBUG_REDUCE_READ_DELAY_US makes rank 1's host read its reduce partials late: a
+# peer's next reduce must not overwrite them (two alternating slot banks).
+@pytest.mark.parametrize("env1", [{}, {"HDA_DEBUG_PULL_DELAY_US": "300", "HDA_DEBUG_REDUCE_READ_DELAY_US": "50000"},
                                   {"HDA_DEBUG_PULL_DELAY_US": "300", "HDA_HALO_MODE": "1"}],
                          ids=["plain", "slow-reader", "slow-reader-fused"])
 def test_spmd_two_gpus(env1):

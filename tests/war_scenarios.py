@@ -1,0 +1,121 @@
+"""WAR-race scenarios run in a subprocess (the delay hooks are read once per process).
+
+    python tests/war_scenarios.py pull_war <n_gpus>
+    python tests/war_scenarios.py staged_regrow <n_gpus>
+
+Each prints "OK" or a mismatch description and exits 0 / 1.  Test code only: the
+library runs the program, the oracle replays it, every replica is compared bit for bit.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_1809_05657_b200 as H  # noqa: E402
+import synth  # noqa: E402
+
+
+def _compare(h, w, arrs, P):
+    bad = []
+    for a in arrs:
+        if not (h.owner_map(a) == w.owner_map(a)).all():
+            bad.append(f"array {a}: owner map")
+        for d in range(P):
+            if h.read_replica(a, d).tobytes() != w.replica(a, d).tobytes():
+                bad.append(f"array {a} device {d}: replica differs")
+    return bad
+
+
+def pull_war(G):
+    """Three devices, reader-side WAR: q=0 writes rows 0-3 of X; r=1 pulls
+    them from q (r's pulls sleep, HDA_DEBUG_PULL_DELAY_DEV=1); p=2 redefines them
+    (waiting on no one: r read q's replica, not p's); then q pulls them back from p
+    into its own replica.  Unless q's pull waits for r's ACK, r reads p's new values
+    out of q's replica and its copy Y differs from the oracle's."""
+    P, shape = 3, (12, 64)
+    h = H.HDArray(n_gpus=G, n_devices=P)
+    w = O.Oracle(P)
+    x0 = synth.uniform(21, shape)
+    empty = ([0, 0], [0, 0])
+
+    def manual(be, rows):  # device d works on rows[d] (None = empty region)
+        lbs, ubs = [], []
+        for r in rows:
+            if r is None:
+                lbs.append(list(empty[0]))
+                ubs.append(list(empty[1]))
+            else:
+                lbs.append([r[0], 0])
+                ubs.append([r[1], shape[1]])
+        return be.partition_manual(shape, lbs, ubs)
+
+    parts = {}
+    for be in (h, w):
+        X, Y, Z = (be.create(H.F64, shape) for _ in range(3))
+        D = manual(be, [(0, 4), (4, 8), (8, 12)])
+        W1 = manual(be, [None, (0, 4), None])
+        W2 = manual(be, [None, None, (0, 4)])
+        W3 = manual(be, [(0, 4), None, None])
+        parts[be] = (X, Y, Z, D, W1, W2, W3)
+    bad = []
+    for it in range(3):
+        for be in (h, w):
+            X, Y, Z, D, W1, W2, W3 = parts[be]
+            be.write(X, D, x0 + it)
+            be.apply(H.K_COPY, W1, [(Y, [], [(0, 0)]), (X, [(0, 0)], [])])             # r pulls from q
+            be.apply(H.K_STAMP, W2, [(X, [], [(0, 0)])], [float(100 + it)])            # p redefines
+            be.apply(H.K_COPY, W3, [(Z, [], [(0, 0)]), (X, [(0, 0)], [])])             # q pulls from p
+        X, Y, Z = parts[h][:3]
+        bad += [f"it{it}: {b}" for b in _compare(h, w, [X, Y, Z], P)]
+    h.close()
+    return bad
+
+
+def staged_regrow(G):
+    """STAGED transport: a cached small-message plan (Jacobi halos) is
+    replayed after a larger plan (a ROW->COL repartition with 2 MiB blocks) has grown
+    the staging buffers; the replay must use the new buffers."""
+    P = 2
+    h = H.HDArray(n_gpus=G, n_devices=P)
+    h.set_transport(1)
+    w = O.Oracle(P)
+    J = [(0, -1), (0, 1), (-1, 0), (1, 0)]
+    shape, big = (34, 130), (1024, 1024)
+    u0, v0 = synth.uniform(3, shape), synth.uniform(4, big, "f32")
+    arrs = {}
+    for be in (h, w):
+        Xa, Ya = be.create(H.F64, shape, u0), be.create(H.F64, shape, u0)
+        part = be.partition(H.ROW, shape, (1, 1), (shape[0] - 1, shape[1] - 1))
+        Zb = be.create(H.F32, big)
+        rp, cp = be.partition(H.ROW, big), be.partition(H.COL, big)
+        be.write(Zb, rp, v0)
+        arrs[be] = (Xa, Ya, part, Zb, rp, cp)
+
+    def jacobi(n):
+        for s in range(n):
+            for be in (h, w):
+                Xa, Ya, part = arrs[be][:3]
+                src, dst = (Xa, Ya) if s % 2 == 0 else (Ya, Xa)
+                be.apply(H.K_JACOBI5, part, [(dst, [], [(0, 0)]), (src, J, [])])
+
+    jacobi(6)                       # small plans cached, staging at its 1 MiB minimum
+    for be in (h, w):
+        Zb, rp, cp = arrs[be][3:]
+        be.apply(H.K_SCALE, cp, [(Zb, [(0, 0)], [(0, 0)])], [2.0])   # 2 MiB blocks: regrow
+        be.apply(H.K_SCALE, rp, [(Zb, [(0, 0)], [(0, 0)])], [0.5])
+    jacobi(6)                       # cached small plans replayed
+    Xa, Ya, _, Zb = arrs[h][:4]
+    bad = _compare(h, w, [Xa, Ya, Zb], P)
+    h.close()
+    return bad
+
+
+if __name__ == "__main__":
+    name, G = sys.argv[1], int(sys.argv[2])
+    bad = {"pull_war": pull_war, "staged_regrow": staged_regrow}[name](G)
+    print("OK" if not bad else "MISMATCH " + "; ".join(bad[:8]))
+    sys.exit(1 if bad else 0)
