@@ -597,6 +597,11 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
                                       const int64_t* const* ubs, int nb, const KSync& ks, cudaStream_t s) {
   const int64_t ld = shape[2];
   constexpr int V = V16<T>::n;
+  if (nb == 1 && stencil_tma_mode() >= (KIND == 1 ? 1 : 2)) {
+    const cudaError_t e = launch_stencil2d_tma(KIND, sizeof(T) == 8 ? 0 : 1, in, out, shape, lbs[0], ubs[0], ks, s);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   const bool vec = (ld * (int64_t)sizeof(T)) % 16 == 0 && ((uintptr_t)in % 16) == 0 &&
                    ((uintptr_t)out % 16) == 0;
   if (vec) {

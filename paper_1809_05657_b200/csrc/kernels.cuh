@@ -97,6 +97,12 @@ struct HaloPull {
 cudaError_t launch_stencil2d_halo(int kernel, int dtype, const void* in, void* out, const int64_t* shape,
                                   const int64_t* const* lbs, const int64_t* const* ubs, int nb, int n_interior,
                                   const RunBatch& pull, const HaloPull& hp, const KSync& ks, cudaStream_t s);
+// TMA-ring 2-D stencil over ONE work box (stencil_tma.cu): kind 0 = JACOBI5, 1 = STENCIL9;
+// cudaErrorNotSupported when the box/layout does not qualify (caller uses the register
+// march).  stencil_tma_mode(): HDA_TMA, 0 off, 1 (default) 9-point only, 2 both.
+cudaError_t launch_stencil2d_tma(int kind, int dtype, const void* in, void* out, const int64_t* shape,
+                                 const int64_t* lb, const int64_t* ub, const KSync& ks, cudaStream_t s);
+int stencil_tma_mode();
 // up to 8 boxes in one launch (flat grid of tiles)
 cudaError_t launch_jacobi5(int dtype, const void* in, void* out, const int64_t* shape,
                            const int64_t* const* lbs, const int64_t* const* ubs, int nb, const KSync& ks,

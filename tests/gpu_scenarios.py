@@ -1,7 +1,9 @@
-"""WAR-race scenarios run in a subprocess (the delay hooks are read once per process).
+"""GPU scenarios run in a subprocess (the delay hooks and kernel switches are read once
+per process): WAR races and the TMA stencil shapes.
 
-    python tests/war_scenarios.py pull_war <n_gpus>
-    python tests/war_scenarios.py staged_regrow <n_gpus>
+    python tests/gpu_scenarios.py pull_war <n_gpus>
+    python tests/gpu_scenarios.py staged_regrow <n_gpus>
+    HDA_TMA=2 python tests/gpu_scenarios.py tma_shapes 1
 
 Each prints "OK" or a mismatch description and exits 0 / 1.  Test code only: the
 library runs the program, the oracle replays it, every replica is compared bit for bit.
@@ -114,8 +116,37 @@ def staged_regrow(G):
     return bad
 
 
+def tma_shapes(G):
+    """TMA-ring 2-D stencils (stencil_tma.cu) on boxes spanning several 252/248-column
+    strips and several row blocks, with ragged ends, boxes that start off the 32-byte
+    strip alignment and partitions whose devices get different tile heights; every
+    replica against the oracle, bit for bit, f64 and f32, 5- and 9-point."""
+    J = [(0, -1), (0, 1), (-1, 0), (1, 0)]
+    N9 = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1) if i or j]
+    bad = []
+    cases = [((517, 1111), 1, (1, 1), None), ((300, 1500), 2, (5, 7), (291, 1433)), ((1000, 600), 3, (1, 3), None),
+             ((133, 2050), 1, (40, 250), (100, 1900))]
+    for dt, name in ((H.F64, "f64"), (H.F32, "f32")):
+        for shape, P, lb, ub in cases:
+            ub = ub or (shape[0] - 1, shape[1] - 1)
+            u0 = synth.uniform(31, shape, name)
+            for K, uses in ((H.K_JACOBI5, J), (H.K_STENCIL9, N9)):
+                h = H.HDArray(n_gpus=G, n_devices=P)
+                w = O.Oracle(P)
+                for be in (h, w):
+                    X = be.create(dt, shape, u0)
+                    Y = be.create(dt, shape, u0)
+                    part = be.partition(H.ROW, shape, lb, ub)
+                    for s in range(3):
+                        src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+                        be.apply(K, part, [(dst, [], [(0, 0)]), (src, uses, [])])
+                bad += [f"{name} {shape} P={P} K={K}: {b}" for b in _compare(h, w, [X, Y], P)]
+                h.close()
+    return bad
+
+
 if __name__ == "__main__":
     name, G = sys.argv[1], int(sys.argv[2])
-    bad = {"pull_war": pull_war, "staged_regrow": staged_regrow}[name](G)
+    bad = {"pull_war": pull_war, "staged_regrow": staged_regrow, "tma_shapes": tma_shapes}[name](G)
     print("OK" if not bad else "MISMATCH " + "; ".join(bad[:8]))
     sys.exit(1 if bad else 0)

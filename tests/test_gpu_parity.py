@@ -586,7 +586,7 @@ def _scenario(name, G, **env):
     import subprocess
     import sys
     e = dict(os.environ, HDA_TIMEOUT_MS="20000", **env)
-    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "war_scenarios.py")
+    script = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gpu_scenarios.py")
     return subprocess.run([sys.executable, script, name, str(G)], env=e, capture_output=True, text=True,
                           timeout=600)
 
@@ -613,4 +613,13 @@ def test_staged_plan_replay_after_regrow(G):
     if ngpus() < G:
         pytest.skip(f"needs {G} GPUs")
     r = _scenario("staged_regrow", G)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_stencil2d_tma_shapes(mode):
+    """The TMA-ring 2-D stencils (HDA_TMA=1: 9-point, 2: both, 0: register march only)
+    on multi-strip, multi-row-block boxes with ragged and unaligned edges, bit-exact
+    against the oracle for every replica."""
+    r = _scenario("tma_shapes", 1, HDA_TMA=mode)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
