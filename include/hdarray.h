@@ -161,6 +161,8 @@ typedef struct {
   int64_t last_bytes;       /* payload bytes of the last call */
   int64_t kernel_launches;  /* CUDA kernels launched by this process, cumulative */
   double tracker_us;        /* host time in compose/plan/commit/cache, cumulative */
+  int64_t gated_products;   /* GEMM launches gated on their B rows' arrival (all-gather
+                               overlapped with the product), cumulative */
 } hda_stats_t;
 
 /* ---- lifetime (Table 2 Init/Exit) ----

@@ -31,7 +31,7 @@ cudaError_t launch_gemm_simt(int c_dtype, const void* A, const void* B, void* C,
                              cudaStream_t s);
 cudaError_t launch_gemm_2sm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                             const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
-                            cudaStream_t s);
+                            cudaStream_t s, const KGate* gate);
 
 namespace tc {
 
@@ -270,9 +270,10 @@ static int sm_count() {
 
 cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                         const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
-                        cudaStream_t s) {
+                        cudaStream_t s, const KGate* gate) {
   const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
   if (m0 >= m1 || n0 >= n1) return cudaSuccess;
+  const bool gated = gate && gate->n > 0;
   // CTA-pair kernel (gemm_tcgen05_2sm.cu) by default: 16384^2 back-to-back 1655-1691
   // vs 1462-1482 TFLOP/s for this single-CTA kernel (HDA_GEMM_2SM=0 selects it)
   static const int two_sm = [] {
@@ -280,9 +281,10 @@ cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int6
     return e ? std::atoi(e) : 1;
   }();
   if (two_sm) {
-    const cudaError_t e = launch_gemm_2sm(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, ks, s);
+    const cudaError_t e = launch_gemm_2sm(c_dtype, A, B, C, M, N, K, lb, ub, alpha, beta, ks, s, gate);
     if (e != cudaErrorNotSupported) return e;
   }
+  if (gated) return cudaErrorNotSupported;
   // TMA needs 16-byte row pitches and aligned bases; tiny problems use the CUDA-core path
   const bool tc_ok = (K % 8 == 0) && (N % 8 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) &&
                      K >= tc::BK && N >= 64 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX;

@@ -11,13 +11,17 @@
 //   warps 4-7  epilogue (both CTAs): each CTA drains its 128 rows of the accumulator
 // Every mbarrier wait is bounded; a timeout aborts the whole grid quickly (wrong
 // results, caught by the parity tests) instead of hanging the GPU.
+// Optionally gated (KGate): B rows still arriving over NVLink are waited for per
+// k-block by the producers, so the all-gather of B overlaps the product.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "sync.cuh"
@@ -112,6 +116,36 @@ __device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, 
       : "memory");
 }
 
+// Gated K (all-gather fused into the product, kernels.cuh KGate): before the first TMA
+// load of k-block kb, wait for every source whose rows [lo, hi) meet it.  `ready` keeps
+// the sources already seen for the rest of the launch.  The acquire of the flag orders
+// the copy-engine writes before it (the stream write that set it carries a system
+// fence); the proxy fence extends that order to the TMA (async proxy) reads that follow.
+__device__ __forceinline__ void gate_wait(const KGate& g, int kb, uint32_t& ready) {
+  const int64_t k0 = (int64_t)kb * BK, k1 = k0 + BK;
+  bool waited = false;
+  for (int i = 0; i < g.n; i++) {
+    if ((ready >> i) & 1u) continue;
+    if (g.lo[i] >= k1 || g.hi[i] <= k0) continue;
+    for (long long spin = 0;; spin++) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(g.flag[i]) : "memory");
+      if (v >= g.val[i]) break;
+      if ((spin & 255) == 255) {
+        if (aborted()) return;
+        if (spin > (1LL << 26)) {  // seconds: the copies never landed; stop the grid
+          atomicExch(&g_abort, 1);
+          return;
+        }
+        __nanosleep(256);
+      }
+    }
+    ready |= 1u << i;
+    waited = true;
+  }
+  if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // D f32, A/B bf16, A K-major, B MN-major, M = 256 (the pair), N = 256
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)((2 * BM) >> 4) << 24);
@@ -149,7 +183,7 @@ template <typename TC>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, TC* C,
                  int64_t N, int64_t K, int64_t m0, int64_t m1, int64_t n0, int64_t n1, int64_t nbase, float alpha,
-                 float beta, const __grid_constant__ KSync ks) {
+                 float beta, const __grid_constant__ KSync ks, const __grid_constant__ KGate gate) {
   ks_pre(ks);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -166,6 +200,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t n_tiles = tiles_m * tiles_n;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int kblocks = (int)((K + BK - 1) / BK);
+  // K segments (KGate): one pass over the tiles per segment when the output is fp32 and
+  // the launch is gated (each pass accumulates into C), else one pass over all of them
+  const bool multi = gate.multi != 0;
+  const int npass = multi ? gate.nseg : 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; s++) {
@@ -195,23 +233,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t full0 = mapa(smem_u32(&full[0]), 0);  // the leader's full[0]
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {  // abort checked per tile only
-        int mt, nt;
-        tile_coords(t, tiles_m, tiles_n, mt, nt);
-        const int row0 = (int)(m0 + (int64_t)mt * 2 * BM + rank * BM);
-        const int col0 = (int)(nbase + (int64_t)nt * BN + rank * BNH);
-        for (int kb = 0; kb < kblocks; kb++) {
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* sa = smem + s * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
-          const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
-          tma_load_2sm(sa, &map_a, fb, kb * BK, row0);
+      uint32_t ready = 0;
+      for (int pp = 0; pp < npass && !aborted(); pp++) {
+        for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {  // abort checked per tile only
+          int mt, nt;
+          tile_coords(t, tiles_m, tiles_n, mt, nt);
+          const int row0 = (int)(m0 + (int64_t)mt * 2 * BM + rank * BM);
+          const int col0 = (int)(nbase + (int64_t)nt * BN + rank * BNH);
+          // K order: the segments of this pass (all of them when one pass covers K); the
+          // MMA issuer only counts blocks, so the order changes nothing else
+          for (int sg = multi ? pp : 0; sg < (multi ? pp + 1 : gate.nseg); sg++) {
+            for (int kb = gate.skb0[sg]; kb < gate.skb1[sg]; kb++) {
+              if (gate.n > 0) gate_wait(gate, kb, ready);
+              mbar_wait(&empty[s], ph ^ 1);
+              uint8_t* sa = smem + s * STAGE_BYTES;
+              uint8_t* sb = sa + A_BYTES;
+              if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+              const uint32_t fb = full0 + (uint32_t)(s * sizeof(uint64_t));
+              tma_load_2sm(sa, &map_a, fb, kb * BK, row0);
 #pragma unroll
-          for (int j = 0; j < BNH / 64; j++) tma_load_2sm(sb + j * (BK * 128), &map_b, fb, col0 + 64 * j, kb * BK);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+              for (int j = 0; j < BNH / 64; j++)
+                tma_load_2sm(sb + j * (BK * 128), &map_b, fb, col0 + 64 * j, kb * BK);
+              if (++s == STAGES) {
+                s = 0;
+                ph ^= 1;
+              }
+            }
           }
         }
       }
@@ -222,31 +269,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
-        mbar_wait<true>(&tempty[acc], aph ^ 1);  // arrivals from both CTAs' epilogues
-        fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < kblocks; kb++) {
-          mbar_wait(&full[s], ph);
+      for (int pp = 0; pp < npass && !aborted(); pp++) {
+        const int nkb = multi ? gate.skb1[pp] - gate.skb0[pp] : kblocks;
+        for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
+          mbar_wait<true>(&tempty[acc], aph ^ 1);  // arrivals from both CTAs' epilogues
           fence_after();
-          const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t b_addr = a_addr + A_BYTES;
+          const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+          for (int i = 0; i < nkb; i++) {
+            mbar_wait(&full[s], ph);
+            fence_after();
+            const uint32_t a_addr = smem_u32(smem + s * STAGE_BYTES);
+            const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / UK; k++) {
-            const uint64_t ad = smem_desc(a_addr + k * (UK * 2), 16, 1024);
-            const uint64_t bd = smem_desc(b_addr + k * (UK * 128), BK * 128, 1024);
-            mma2(tmem_d, ad, bd, (kb | k) != 0);
+            for (int k = 0; k < BK / UK; k++) {
+              const uint64_t ad = smem_desc(a_addr + k * (UK * 2), 16, 1024);
+              const uint64_t bd = smem_desc(b_addr + k * (UK * 128), BK * 128, 1024);
+              mma2(tmem_d, ad, bd, (i | k) != 0);
+            }
+            commit_both(&empty[s]);
+            if (++s == STAGES) {
+              s = 0;
+              ph ^= 1;
+            }
           }
-          commit_both(&empty[s]);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+          commit_both(&tfull[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            aph ^= 1;
           }
-        }
-        commit_both(&tfull[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          aph ^= 1;
         }
       }
     }
@@ -255,26 +305,31 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tempty0 = mapa(smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t aph = 0;
-    for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
-      int mt, nt;
-      tile_coords(t, tiles_m, tiles_n, mt, nt);
-      const int64_t row = m0 + (int64_t)mt * 2 * BM + rank * BM + q * 32 + lane;
-      const int64_t colb = nbase + (int64_t)nt * BN;
-      mbar_wait(&tfull[acc], aph);
-      fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+    for (int pp = 0; pp < npass && !aborted(); pp++) {
+      // later passes add their K segment to what the earlier ones stored; the same
+      // thread stores and re-reads each element, so program order suffices
+      const float b = pp == 0 ? beta : 1.f;
+      for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
+        int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, mt, nt);
+        const int64_t row = m0 + (int64_t)mt * 2 * BM + rank * BM + q * 32 + lane;
+        const int64_t colb = nbase + (int64_t)nt * BN;
+        mbar_wait(&tfull[acc], aph);
+        fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; c++) {
-        uint32_t r[32];
-        tmem_ld32(taddr + c * 32, r);
-        if (row < m1) store_chunk<TC>(C + row * N, colb + c * 32, n0, n1, r, alpha, beta);
-      }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
-      if (++acc == 2) {
-        acc = 0;
-        aph ^= 1;
+        for (int c = 0; c < BN / 32; c++) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          if (row < m1) store_chunk<TC>(C + row * N, colb + c * 32, n0, n1, r, alpha, b);
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
       }
     }
   }
@@ -285,13 +340,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(TMEM_COLS));
   }
+  // an aborted grid (a wait that never completed) surfaces as the sticky HDA_ETIMEOUT
+  if (threadIdx.x == 0 && ks.err && aborted()) *reinterpret_cast<volatile int*>(ks.err) = -7;
   ks_post(ks);
 }
 
 template <typename TC>
 static cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, TC* C, int64_t N, int64_t K, int64_t m0,
                             int64_t m1, int64_t n0, int64_t n1, float alpha, float beta, const KSync& ks,
-                            cudaStream_t s, int sms) {
+                            cudaStream_t s, int sms, const KGate& gate) {
   const int64_t nbase = n0 & ~(int64_t)7;  // 16-byte aligned TMA column base (see gemm_tcgen05.cu)
   const int64_t tiles = ((m1 - m0 + 2 * BM - 1) / (2 * BM)) * ((n1 - nbase + BN - 1) / BN);
   const int clusters = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms / 2));
@@ -308,7 +365,7 @@ static cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, TC* C,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm2_kernel<TC>, ma, mb, C, N, K, m0, m1, n0, n1, nbase, alpha, beta, ks);
+  return cudaLaunchKernelEx(&cfg, gemm2_kernel<TC>, ma, mb, C, N, K, m0, m1, n0, n1, nbase, alpha, beta, ks, gate);
 }
 
 }  // namespace tc2
@@ -316,7 +373,7 @@ static cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, TC* C,
 // Returns cudaErrorNotSupported when the 2-SM path does not apply (caller falls back).
 cudaError_t launch_gemm_2sm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N, int64_t K,
                             const int64_t* lb, const int64_t* ub, float alpha, float beta, const KSync& ks,
-                            cudaStream_t s) {
+                            cudaStream_t s, const KGate* gate) {
   const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
   const bool ok = (K % 8 == 0) && (N % 8 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) &&
                   K >= tc2::BK && N >= 128 && M <= INT32_MAX && N <= INT32_MAX && K <= INT32_MAX &&
@@ -328,9 +385,59 @@ cudaError_t launch_gemm_2sm(int c_dtype, const void* A, const void* B, void* C, 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  KGate g;
+  std::memset(&g, 0, sizeof g);
+  const int kblocks = (int)((K + tc2::BK - 1) / tc2::BK);
+  g.nseg = 1;
+  g.skb1[0] = kblocks;
+  if (gate && gate->n > 0) {
+    if (gate->n > kMaxGate) return cudaErrorNotSupported;
+    g = *gate;
+    // segments: k-blocks ordered by the arrival rank of the last source they need
+    // (-1 = resident), ties by k; runs of consecutive k-blocks with one rank
+    std::vector<int> rdy(kblocks, -1);
+    for (int i = 0; i < g.n; i++)
+      for (int64_t kb = g.lo[i] / tc2::BK; kb < kblocks && kb * tc2::BK < g.hi[i]; kb++) rdy[kb] = i;
+    std::vector<int> order(kblocks);
+    for (int kb = 0; kb < kblocks; kb++) order[kb] = kb;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rdy[a] < rdy[b]; });
+    int ns = 0;
+    for (int j = 0; j < kblocks; j++) {
+      const int kb = order[j];
+      if (ns > 0 && g.skb1[ns - 1] == kb && rdy[g.skb0[ns - 1]] == rdy[kb]) {
+        g.skb1[ns - 1] = kb + 1;
+        continue;
+      }
+      if (ns == kMaxGate + 1) return cudaErrorNotSupported;
+      g.skb0[ns] = kb;
+      g.skb1[ns] = kb + 1;
+      ns++;
+    }
+    g.nseg = ns;
+    // per-segment passes: fp32 C only (a bf16 C would be rounded once per pass)
+    static const int multi = [] {
+      const char* e = std::getenv("HDA_GATE_PASSES");
+      return e ? std::atoi(e) : 1;
+    }();
+    g.multi = (multi && c_dtype == 1 && ns > 1) ? 1 : 0;
+  } else {
+    // measurement hook: HDA_DEBUG_GEMM_SEGS=s splits an ungated K into s passes (fp32 C)
+    static const int dbg = [] {
+      const char* e = std::getenv("HDA_DEBUG_GEMM_SEGS");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (dbg > 1 && dbg <= kMaxGate && c_dtype == 1 && kblocks >= dbg) {
+      g.nseg = dbg;
+      g.multi = 1;
+      for (int j = 0; j < dbg; j++) {
+        g.skb0[j] = (int)((int64_t)kblocks * j / dbg);
+        g.skb1[j] = (int)((int64_t)kblocks * (j + 1) / dbg);
+      }
+    }
+  }
   if (c_dtype == 1)
-    return tc2::launch_t<float>(ma, mb, (float*)C, N, K, m0, m1, n0, n1, alpha, beta, ks, s, sms);
-  return tc2::launch_t<__nv_bfloat16>(ma, mb, (__nv_bfloat16*)C, N, K, m0, m1, n0, n1, alpha, beta, ks, s, sms);
+    return tc2::launch_t<float>(ma, mb, (float*)C, N, K, m0, m1, n0, n1, alpha, beta, ks, s, sms, g);
+  return tc2::launch_t<__nv_bfloat16>(ma, mb, (__nv_bfloat16*)C, N, K, m0, m1, n0, n1, alpha, beta, ks, s, sms, g);
 }
 
 }  // namespace hda

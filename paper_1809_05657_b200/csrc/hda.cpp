@@ -20,6 +20,7 @@
 // 1-block spin kernels with a timeout (sticky HDA_ETIMEOUT, never a hang); signals
 // are release stores at system scope.  Devices that share a CUDA stream (virtual
 // devices on one GPU) are ordered by the stream and skip both.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,7 +54,8 @@ constexpr int SW_RED = 256, SW_REDSIG = 320;  // reduce partials [P] and their e
 constexpr int SW_DEBUG = 195;                  // measurement hooks only
 constexpr int SW_SCRATCH = 384;               // kReduceBlocks partials
 constexpr int SW_RED_B = SW_SCRATCH + kReduceBlocks;  // second bank of reduce partials [P]
-constexpr int SW_WORDS = SW_RED_B + 64;
+constexpr int SW_GATE = SW_RED_B + 64;  // [P] local: epoch at which source p's gated GEMM rows landed
+constexpr int SW_WORDS = SW_GATE + 64;
 constexpr uint32_t BLOB_MAGIC = 0x48444131u;  // "HDA1"
 constexpr int64_t kCeBytes = 1 << 20;         // AUTO: messages >= 1 MiB go to the copy engine
 
@@ -97,6 +99,13 @@ struct PullJob {
   bool split = false;
   std::vector<Box> interior, dependent;
   std::vector<cudaMemcpy3DParms> ce;  // AUTO transport: bulk messages on the copy engine
+  std::vector<int> ce_src;            // source device of each ce copy
+  // GEMM whose incoming messages are whole row blocks of B, all on the copy engine: the
+  // product runs gated on their arrival (KGate) instead of after a join; rows [lo, hi)
+  // of B per srcs[i]
+  bool gate = false;
+  std::vector<std::pair<int64_t, int64_t>> gate_rows;
+  int64_t gate_k = 0;  // rows of B (the product's K)
 };
 struct PendEntry {
   int array, src, dst;
@@ -230,6 +239,8 @@ struct hda_ctx {
   std::vector<char> pulled_on_comm;  // [P] this call's pull for device q ran on the comm stream
   std::vector<const PullJob*> cur_pull;
   std::vector<const PullJob*> halo_job;  // [P] pull deferred into the fused halo-stencil launch
+  std::vector<KGate> gate;               // [P] this call's gated product (issue_gated_pull)
+  std::vector<char> gated;               // [P] gate[q] is armed for this call
   std::vector<TimedEv> tev;
   std::vector<cudaEvent_t> ev_pool;
   double ktime_ms[KN_COUNT] = {};
@@ -478,6 +489,16 @@ static int ensure_stage(hda_ctx_t* ctx, std::vector<char*>& v, std::vector<size_
   return HDA_OK;
 }
 
+// AUTO transport threshold (HDA_CE_BYTES, default kCeBytes): tests lower it to put
+// small bulk messages on the copy-engine (and gated-product) path
+static int64_t ce_bytes() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("HDA_CE_BYTES");
+    return e ? std::atoll(e) : kCeBytes;
+  }();
+  return v;
+}
+
 static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
   const int P = ctx->P;
   ep.staged = ctx->transport == HDA_XPORT_STAGED;
@@ -514,7 +535,7 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
         d.dst = ctx->arr[m.array].ptr[q];
         if (!d.src || !d.dst) return fail(ctx, HDA_ESTATE, "replica not mapped (SPMD handles missing?)");
         const int64_t bytes = box_volume(m.box) * (int64_t)a.es;
-        if (ctx->transport == HDA_XPORT_AUTO && bytes >= kCeBytes && !same_stream(ctx, m.src, q)) {
+        if (ctx->transport == HDA_XPORT_AUTO && bytes >= ce_bytes() && !same_stream(ctx, m.src, q)) {
           // bulk: copy-engine peer copy of the strided box (no SM time, no staging)
           cudaMemcpy3DParms p;
           std::memset(&p, 0, sizeof p);
@@ -525,6 +546,7 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
                                      (size_t)(fb.ub[0] - fb.lb[0]));
           p.kind = cudaMemcpyDefault;
           job.ce.push_back(p);
+          job.ce_src.push_back(m.src);
         } else {
           descs.push_back(d);
         }
@@ -538,6 +560,26 @@ static int build_exec(hda_ctx_t* ctx, const Transition* t, ExecPlan& ep) {
         if (!same_stream(ctx, p, q)) job.cross = true;
       // overlap split (footprint radius r of the built-in kernel)
       const CallInfo& ci = *t->info;
+      if (ci.kernel == KN_GEMM && descs.empty() && job.cross && job.srcs.size() <= (size_t)kMaxGate) {
+        // gated product: every message is one full-width row block of B from another GPU
+        const int Barr = ci.param_array[2];
+        const TArray& B = ctx->tr->array(Barr);
+        bool ok = B.ndim == 2;
+        std::vector<std::pair<int64_t, int64_t>> rows(job.srcs.size(), {-1, -1});
+        for (const Msg* mp : mine) {
+          const size_t i = std::find(job.srcs.begin(), job.srcs.end(), mp->src) - job.srcs.begin();
+          if (mp->array != Barr || same_stream(ctx, mp->src, q) || rows[i].first >= 0 || mp->box.lb[1] != 0 ||
+              mp->box.ub[1] != B.shape[1])
+            ok = false;
+          else
+            rows[i] = {mp->box.lb[0], mp->box.ub[0]};
+        }
+        if (ok) {
+          job.gate = true;
+          job.gate_rows = rows;
+          job.gate_k = B.shape[0];
+        }
+      }
       int r = -1;
       if (ci.kernel == KN_JACOBI5 || ci.kernel == KN_STENCIL9 || ci.kernel == KN_STENCIL7_3D) r = 1;
       if (ci.kernel == KN_SCALE || ci.kernel == KN_COPY) r = 0;
@@ -750,7 +792,98 @@ static int exchange_plan(hda_ctx_t* ctx, const Transition* t, unsigned long long
 static void war_waits(hda_ctx_t* ctx, const CallInfo& ci, int q, KSync& ks);
 static bool war_disjoint(hda_ctx_t* ctx, const CallInfo& ci, int q, const std::vector<Box>& boxes);
 static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
-                      const std::vector<Box>* boxes = nullptr, cudaStream_t stream = nullptr);
+                      const std::vector<Box>* boxes = nullptr, cudaStream_t stream = nullptr,
+                      const KGate* gate = nullptr);
+
+// Stream memory operations (driver API, no SM time): the gated product's comm stream
+// waits for the sources' PROD words and publishes arrivals and ACKs without a kernel, so
+// it makes progress while the GPU-filling GEMM spins on the arrival flags.
+typedef CUresult (*StreamValue64Fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*DeviceAttrFn)(int*, CUdevice_attribute, CUdevice);
+struct MemOps {
+  StreamValue64Fn wait = nullptr, write = nullptr;
+  bool ok = false;
+};
+static const MemOps& memops() {
+  static const MemOps m = [] {
+    MemOps r;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      r.wait = (StreamValue64Fn)p;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      r.write = (StreamValue64Fn)p;
+    int attr = 0, dev = 0;
+    if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess && cudaGetDevice(&dev) == cudaSuccess)
+      ((DeviceAttrFn)p)(&attr, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, (CUdevice)dev);
+    r.ok = r.wait && r.write && attr;
+    return r;
+  }();
+  return m;
+}
+#define CU(call)                                                              \
+  do {                                                                        \
+    const CUresult cr_ = (call);                                              \
+    if (cr_ != CUDA_SUCCESS) return fail(ctx, HDA_ECUDA, "stream memory op failed: " #call); \
+  } while (0)
+
+// HDA_GEMM_GATE (default 0, opt-in): a GEMM whose B rows arrive from other GPUs runs
+// gated on their arrival (all-gather overlapped with the product) instead of after a
+// join.  Measured slower on B200 (2MM ROW 16384^2 at N=2: 5.62-5.70 ms per step gated vs
+// 5.40 joined): the 256 MiB copy takes 0.43 ms either way, but the gated
+// product runs 0.68 ms longer.  Two passes cost 0.1-0.25 ms on their own (the second
+// re-reads and re-writes the fp32 C; HDA_DEBUG_GEMM_SEGS), a concurrent copy slows a
+// product by 0-0.17 ms (tools/ce_contention.py); the rest is not accounted for.
+static bool gate_enabled() {
+  static const int v = env_int("HDA_GEMM_GATE", 0);
+  return v != 0;
+}
+
+// The gated product's exchange (reader q): on the comm stream, forked after everything
+// issued before this call, per source in the permutation order (q+1, q+2, ...): wait for
+// its PROD word, copy its row block of B on the copy engine, then publish the arrival
+// flag (local) and the source's ACK.  The GEMM on the main stream starts at once with
+// the resident rows and waits per k-block (KGate).
+static int issue_gated_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k) {
+  const int q = job.dst;
+  const MemOps& mo = memops();
+  CK(cudaSetDevice(ordinal_of(ctx, q)));
+  Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+  CK(cudaEventRecord(g.ev_fork, g.stream));
+  CK(cudaStreamWaitEvent(g.comm, g.ev_fork, 0));
+  ctx->pulled_on_comm[q] = 1;
+  const CUstream cs = (CUstream)g.comm;
+  // WAR: peers that pulled these cells of q's replica earlier must be done reading
+  for (const auto& e : ctx->pull_war[q]) CU(mo.wait(cs, (CUdeviceptr)e.first, e.second, CU_STREAM_WAIT_VALUE_GEQ));
+  cudaEvent_t a = nullptr;
+  int rc;
+  if ((rc = timed_begin(ctx, g.comm, &a))) return rc;
+  KGate& kg = ctx->gate[q];
+  std::memset(&kg, 0, sizeof kg);
+  for (size_t i = 0; i < job.srcs.size(); i++) {
+    const int p = job.srcs[i];
+    if (ctx->last_prod[p])
+      CU(mo.wait(cs, (CUdeviceptr)(ctx->dev[q].sync + SW_PROD + p), ctx->last_prod[p], CU_STREAM_WAIT_VALUE_GEQ));
+    for (size_t c = 0; c < job.ce.size(); c++)
+      if (job.ce_src[c] == p) CK(cudaMemcpy3DAsync(&job.ce[c], g.comm));
+    // default flags: a system-wide fence precedes each write
+    CU(mo.write(cs, (CUdeviceptr)(ctx->dev[q].sync + SW_GATE + p), k, CU_STREAM_WRITE_VALUE_DEFAULT));
+    CU(mo.write(cs, (CUdeviceptr)(ctx->dev[p].sync + SW_ACK + q), k, CU_STREAM_WRITE_VALUE_DEFAULT));
+    kg.lo[i] = job.gate_rows[i].first;
+    kg.hi[i] = job.gate_rows[i].second;
+    kg.flag[i] = ctx->dev[q].sync + SW_GATE + p;
+    kg.val[i] = k;
+  }
+  kg.n = (int32_t)job.srcs.size();  // arrival order = issue order; the launcher derives the K segments
+  mark(ctx, q, 0);
+  if ((rc = timed_end(ctx, g.comm, -100, a))) return rc;
+  CK(cudaEventRecord(g.ev_pull, g.comm));
+  ctx->gated[q] = 1;
+  return HDA_OK;
+}
 
 // one device's pull (reader q = job.dst): thread-safe against the other devices' issue
 static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigned long long k, bool overlap_kernel,
@@ -765,6 +898,7 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
     ctx->halo_job[q] = &job;
     return HDA_OK;
   }
+  if (ctx->overlap && job.gate && gate_enabled() && memops().ok) return issue_gated_pull(ctx, job, k);
   const bool comm = ctx->overlap && job.cross && job.split && overlap_kernel;
   cudaStream_t st = comm ? g.comm : g.stream;
   // Stencils on the comm path: when the interior part touches no cell a peer pulled
@@ -1004,7 +1138,7 @@ static KSync ks_part(hda_ctx_t* ctx, const KSync& ks, bool first, bool last) {
 }
 
 static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
-                      const std::vector<Box>* boxes, cudaStream_t stream) {
+                      const std::vector<Box>* boxes, cudaStream_t stream, const KGate* gate) {
   const CallInfo& ci = *t->info;
   const TPart& pt = ctx->tr->part(ci.part);
   const int X0 = ci.param_array[0];
@@ -1103,8 +1237,15 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
     case KN_GEMM: {
       const TArray& A = ctx->tr->array(ci.param_array[1]);
       const TArray& B = ctx->tr->array(ci.param_array[2]);
-      CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], A.shape[1], fb.lb, fb.ub,
-                     (float)scalars[0], (float)scalars[1], ks, s));
+      cudaError_t e = launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], A.shape[1], fb.lb, fb.ub,
+                                  (float)scalars[0], (float)scalars[1], ks, s, gate);
+      if (e == cudaSuccess && gate) __atomic_fetch_add(&ctx->stats.gated_products, (int64_t)1, __ATOMIC_RELAXED);
+      if (e == cudaErrorNotSupported && gate) {  // no gated kernel for this shape: join the copies
+        CK(cudaStreamWaitEvent(s, ctx->gpus[ctx->dev[q].gpu].ev_pull, 0));
+        e = launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], A.shape[1], fb.lb, fb.ub,
+                        (float)scalars[0], (float)scalars[1], ks, s);
+      }
+      CK(e);
       break;
     }
     default:
@@ -1340,6 +1481,18 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
     count_launch(ctx);
     mark(ctx, q, 1);
     if ((rc = timed_end(ctx, st, kernel, a, 1))) return rc;
+  } else if (kern && ctx->gated[q]) {
+    // gated product: starts at once on the main stream, waits per k-block for the rows
+    // the comm stream is still copying; joined right after (the next call's work)
+    ctx->gated[q] = 0;
+    Gpu& g = ctx->gpus[ctx->dev[q].gpu];
+    cudaEvent_t a;
+    if ((rc = timed_begin(ctx, g.stream, &a))) return rc;
+    if ((rc = run_kernel(ctx, t, q, scalars, ks, nullptr, nullptr, &ctx->gate[q]))) return rc;
+    mark(ctx, q, 1);
+    if ((rc = timed_end(ctx, g.stream, kernel, a))) return rc;
+    CK(cudaStreamWaitEvent(g.stream, g.ev_pull, 0));
+    ctx->pulled_on_comm[q] = 0;
   } else if (kern && ctx->pulled_on_comm[q]) {
     if ((rc = issue_overlapped(ctx, t, q, kernel, scalars, ks))) return rc;
   } else if (kern) {
@@ -1458,6 +1611,8 @@ static hda_ctx_t* new_ctx(int P) {
   ctx->pulled_on_comm.assign(P, 0);
   ctx->cur_pull.assign(P, nullptr);
   ctx->halo_job.assign(P, nullptr);
+  ctx->gate.assign(P, KGate{});
+  ctx->gated.assign(P, 0);
   ctx->split_mode.assign(P, 0);
   ctx->pull_war.assign(P, {});
   ctx->war_done.assign(P, 0);

@@ -125,10 +125,30 @@ cudaError_t launch_reduce(int dtype, const void* x, const int64_t* shape, const 
 // SPMD combine: copy *local (8 bytes) to every peer slot, then release `val` to their flags
 cudaError_t launch_share(const unsigned long long* local, const SignalList& slots, const SignalList& flags,
                          cudaStream_t s);
+// All-gather fused into the product (P:L424's B all-gather; 2MM's D): rows
+// [lo[i], hi[i]) of B arrive from source i while the GEMM runs, and flag[i] reaches
+// val[i] once they have landed in this replica (a stream write after the copy-engine
+// copy).  The producers wait for a source's flag before the first TMA load that touches
+// its rows.  K is walked in segments [skb0[j], skb1[j]) (k-blocks of 64, together
+// exactly [0, K/64)), resident rows first, then the sources in arrival order.  multi:
+// one pass over all output tiles per segment, each pass adding its partial product to C
+// (fp32 C only), so the resident rows' work covers the first copies instead of every
+// tile stalling on its first remote k-block.  n == 0: no gating.
+constexpr int kMaxGate = 16;
+struct KGate {
+  int32_t n, nseg, multi, pad_;
+  int64_t lo[kMaxGate], hi[kMaxGate];
+  const unsigned long long* flag[kMaxGate];
+  unsigned long long val[kMaxGate];
+  int32_t skb0[kMaxGate + 1], skb1[kMaxGate + 1];
+};
+
 // C[rows lb0..ub0, cols lb1..ub1] = alpha * A@B + beta*C ; A [M,K] bf16 row-major,
-// B [K,N] bf16 row-major, C [M,N] f32 or bf16 row-major (full-array strides)
+// B [K,N] bf16 row-major, C [M,N] f32 or bf16 row-major (full-array strides).
+// A gated launch (gate && gate->n > 0) runs only on the CTA-pair kernel:
+// cudaErrorNotSupported otherwise, and the caller joins the copies and launches ungated.
 cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int64_t M, int64_t N,
                         int64_t K, const int64_t* lb, const int64_t* ub, float alpha, float beta,
-                        const KSync& ks, cudaStream_t s);
+                        const KSync& ks, cudaStream_t s, const KGate* gate = nullptr);
 
 }  // namespace hda

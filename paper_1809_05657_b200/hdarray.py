@@ -46,7 +46,8 @@ class hda_msg_t(ctypes.Structure):
 class hda_stats_t(ctypes.Structure):
     _fields_ = [("n_apply", ctypes.c_int64), ("plan_hits", ctypes.c_int64), ("plan_misses", ctypes.c_int64),
                 ("msgs_total", ctypes.c_int64), ("bytes_total", ctypes.c_int64), ("last_msgs", ctypes.c_int64),
-                ("last_bytes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64), ("tracker_us", ctypes.c_double)]
+                ("last_bytes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64), ("tracker_us", ctypes.c_double),
+                ("gated_products", ctypes.c_int64)]
 
 
 EXPORTS = [

@@ -13,6 +13,9 @@ and the CUDA side can be fed identical bits.  Recipes:
 * ``eigenmode2d / eigenmode3d`` — Dirichlet eigenmodes with a zero ghost ring.
 * ``harmonic2d / harmonic3d`` — integer discrete-harmonic fields (fixed points).
 * ``int_bf16(seed, shape, lo, hi)`` — integer matrices stored as bf16 bit patterns.
+* ``special_values(seed, shape, dtype)`` — ``uniform`` in [-1, 1) with about one cell in
+  eight replaced by +Inf, +-0, subnormals, tiny or huge normals (no -Inf, so no stencil
+  sum is Inf - Inf = NaN, whose bit pattern differs between x86 and the GPU).
 * Standard seed of config i: ``SEED0 + i`` (SEED0 = 180905657).
 """
 from __future__ import annotations
@@ -120,3 +123,21 @@ def harmonic3d(n0: int, n1: int, n2: int, dtype=np.float32) -> np.ndarray:
     y = np.arange(n1, dtype=np.int64)[None, :, None]
     x = np.arange(n2, dtype=np.int64)[None, None, :]
     return np.ascontiguousarray((z * z + y * y - 2 * x * x).astype(dtype))
+
+
+def special_values(seed: int, shape, dtype: str = "f64") -> np.ndarray:
+    """uniform(seed) mapped to [-1, 1), with cells whose hash byte selects a special
+    value: +Inf, +0, -0, the smallest subnormal, a mid subnormal, a tiny normal, a huge
+    normal (positive and negative).  Edge cases of constant-weight divisions."""
+    npdt = np.float64 if dtype == "f64" else np.float32
+    u = uniform(seed, shape, dtype).astype(npdt) * npdt(2) - npdt(1)
+    sel = (_hash(seed + 7, shape) >> np.uint64(56)).astype(np.int64)
+    fi = np.finfo(npdt)
+    specials = [np.inf, 0.0, -0.0, fi.smallest_subnormal, fi.smallest_normal * npdt(0.3),
+                fi.smallest_normal * npdt(4), fi.max / npdt(64), -fi.max / npdt(64),
+                fi.smallest_normal * npdt(2**30), -fi.smallest_normal * npdt(2**20)]
+    for k, v in enumerate(specials):
+        u[sel == 200 + 5 * k] = npdt(v)
+        u[sel == 201 + 5 * k] = npdt(v)
+        u[sel == 202 + 5 * k] = npdt(v)
+    return u

@@ -1,9 +1,10 @@
 """GPU scenarios run in a subprocess (the delay hooks and kernel switches are read once
-per process): WAR races and the TMA stencil shapes.
+per process): WAR races, the TMA stencil shapes, the gated product.
 
     python tests/gpu_scenarios.py pull_war <n_gpus>
     python tests/gpu_scenarios.py staged_regrow <n_gpus>
     HDA_TMA=2 python tests/gpu_scenarios.py tma_shapes 1
+    HDA_CE_BYTES=262144 python tests/gpu_scenarios.py gemm_gate <n_gpus>
 
 Each prints "OK" or a mismatch description and exits 0 / 1.  Test code only: the
 library runs the program, the oracle replays it, every replica is compared bit for bit.
@@ -145,8 +146,47 @@ def tma_shapes(G):
     return bad
 
 
+def gemm_gate(G):
+    """2MM under ROW: D = A x B, E = C x D on P = G GPUs.  Every incoming
+    message is a full-width row block of B (call 1) or D (every call) from another GPU
+    on the copy engine, so the product runs gated on their arrival (KGate, own rows
+    first) instead of after a join.  Integer bf16 inputs in [-1, 1]: D rounds to bf16
+    the same way on both sides and |E| <= 2^20, so E (fp32) is exact in any k order and
+    every replica must equal the oracle's bit for bit.  HDA_GEMM_GATE=0 (the default)
+    runs the same program joined (the A/B).  Exits nonzero on a mismatch or when no product was gated
+    though gating is on."""
+    P, S = G, H.STAR
+    bad, gated = [], 0
+    # 1024: k-block aligned row blocks; 1064: blocks of 532 / 266 rows, so k-blocks
+    # straddle two sources (or own rows and a source) and the segments are ragged
+    for n in (1024, 1064):
+        Ab, Bb, Cb = (synth.int_bf16(70 + i, (n, n), -1, 1) for i in range(3))
+        h = H.HDArray(n_gpus=G, n_devices=P)
+        w = O.Oracle(P)
+        for be in (h, w):
+            A, B, C, D = (be.create(H.BF16, (n, n)) for _ in range(4))
+            E = be.create(H.F32, (n, n))
+            part = be.partition(H.ROW, (n, n))
+            for X, v in ((A, Ab), (B, Bb), (C, Cb)):
+                be.write(X, part, v)
+            for it in range(3):
+                be.apply(H.K_GEMM, part, [(D, [], [(0, 0)]), (A, [(0, S)], []), (B, [(S, 0)], [])], [1.0, 0.0])
+                be.apply(H.K_GEMM, part, [(E, [], [(0, 0)]), (C, [(0, S)], []), (D, [(S, 0)], [])], [1.0, 0.0])
+        bad += [f"n={n}: {b}" for b in _compare(h, w, [B, D, E], P)]
+        gated += h.stats()["gated_products"]
+        h.close()
+    # the gated kernel is the CTA-pair one (HDA_GEMM_2SM=0 selects the single-CTA kernel)
+    on = os.environ.get("HDA_GEMM_GATE", "0") != "0" and os.environ.get("HDA_GEMM_2SM", "1") != "0"
+    want = 2 * 4 * P if on else 0  # per size: B once, D three times, on every device
+    if gated != want:
+        bad.append(f"gated products {gated}, expected {want}")
+    print(f"gated products: {gated}")
+    return bad
+
+
 if __name__ == "__main__":
     name, G = sys.argv[1], int(sys.argv[2])
-    bad = {"pull_war": pull_war, "staged_regrow": staged_regrow, "tma_shapes": tma_shapes}[name](G)
+    bad = {"pull_war": pull_war, "staged_regrow": staged_regrow, "tma_shapes": tma_shapes,
+           "gemm_gate": gemm_gate}[name](G)
     print("OK" if not bad else "MISMATCH " + "; ".join(bad[:8]))
     sys.exit(1 if bad else 0)

@@ -162,6 +162,31 @@ def test_stencil7_3d_bit_exact(H, dtype):
     h.close()
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_stencil_division_edge_values(H, dtype):
+    """Stencils on fields with +Inf, signed zeros, subnormals, tiny and huge normals
+    mixed into uniform data (the divisions by 20 and 6 on their slow paths, Inf
+    propagation, sign of zero): every replica bit-identical to the oracle.  2-D boxes
+    large enough for the TMA kernel (ROW) and small enough for the register march (COL,
+    4 devices)."""
+    DT = H.F64 if dtype == "f64" else H.F32
+    cases = [((90, 420), "ROW", 2, H.K_STENCIL9, N9), ((37, 53), "COL", 4, H.K_STENCIL9, N9),
+             ((20, 26, 140), "ROW", 2, H.K_STENCIL7_3D, N7)]
+    for i, (shape, kind, P, K, uses) in enumerate(cases):
+        u0 = synth.special_values(synth.SEED0 + 40 + i, shape, dtype)
+        h = H.HDArray(n_gpus=1, n_devices=P)
+        w = O.Oracle(P)
+        for be in (h, w):
+            X = be.create(DT, shape, u0)
+            Y = be.create(DT, shape, u0)
+            part = be.partition(getattr(H, kind), shape, (1,) * len(shape), tuple(s - 1 for s in shape))
+            for s in range(3):
+                src, dst = (X, Y) if s % 2 == 0 else (Y, X)
+                be.apply(K, part, [(dst, [], [(0,) * len(shape)]), (src, uses, [])])
+        assert_replicas(h, w, [X, Y], P)
+        h.close()
+
+
 # ------------------------------------------------------------------ repartition
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
 @pytest.mark.parametrize("transport", [0, 1])
@@ -613,6 +638,19 @@ def test_staged_plan_replay_after_regrow(G):
     if ngpus() < G:
         pytest.skip(f"needs {G} GPUs")
     r = _scenario("staged_regrow", G)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("gate", ["1", "0"])
+def test_gemm_gated_allgather(G, gate):
+    """The all-gather of B / D fused into the product (2MM ROW on G GPUs, 256 KiB copy
+    threshold so 1024^2 blocks take the copy engine): bit-exact vs the oracle, gated
+    (HDA_GEMM_GATE=1, every incoming row block waited for per k-block inside the GEMM)
+    and joined (0)."""
+    if ngpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    r = _scenario("gemm_gate", G, HDA_GEMM_GATE=gate, HDA_CE_BYTES="262144")
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 

@@ -1,7 +1,8 @@
 """SPMD mode on >= 2 GPUs: one process per GPU (the bench's torchrun layout), peer
 replicas mapped with CUDA IPC, device-side sync words.  Each rank compares its own
 replica with the oracle after every call (bit-exact), for halo exchange (ROW Jacobi,
-BLOCK 9-point with corners) and a ROW<->COL repartition."""
+BLOCK 9-point with corners), a ROW<->COL repartition and the 2MM chain with its
+all-gathers fused into the product."""
 import os
 import socket
 
@@ -26,6 +27,8 @@ def _port():
 def _worker(rank, world, port, q, env1):
     try:
         os.environ["HDA_TIMEOUT_MS"] = "20000"  # a protocol deadlock fails in seconds
+        os.environ["HDA_CE_BYTES"] = "262144"  # 2MM's 512 KiB row blocks on the copy engine (gated product)
+        os.environ["HDA_GEMM_GATE"] = "1"  # opt-in: the gated product is not the default
         if rank == 1:  # rank 1 only: an asymmetric slow reader opens the WAR window
             os.environ.update(env1)
         import torch
@@ -101,6 +104,25 @@ def _worker(rank, world, port, q, env1):
                 be.apply(H.K_SCALE, cp2, [(Z2, [(0, 0)], [(0, 0)])], [2.0])
                 be.apply(H.K_SCALE, rp2, [(Z2, [(0, 0)], [(0, 0)])], [0.5])
         check("bulk-gpu-filling", [Z2])
+        # 2MM under ROW: the B and D all-gathers fused into the product — the
+        # GEMM starts on its own rows and waits per k-block for the copy-engine blocks
+        # (stream-written arrival flags, no SM time on the comm stream); integer inputs
+        # keep E exact in any k order
+        n2, S = 1024, H.STAR
+        Ab, Bb, Cb = (synth.int_bf16(70 + i, (n2, n2), -1, 1) for i in range(3))
+        g0 = h.stats()["gated_products"]
+        for be in (h, w):
+            GA, GB, GC, GD = (be.create(H.BF16, (n2, n2)) for _ in range(4))
+            GE = be.create(H.F32, (n2, n2))
+            gp = be.partition(H.ROW, (n2, n2))
+            for Xg, v in ((GA, Ab), (GB, Bb), (GC, Cb)):
+                be.write(Xg, gp, v)
+            for it in range(2):
+                be.apply(H.K_GEMM, gp, [(GD, [], [(0, 0)]), (GA, [(0, S)], []), (GB, [(S, 0)], [])], [1.0, 0.0])
+                be.apply(H.K_GEMM, gp, [(GE, [], [(0, 0)]), (GC, [(0, S)], []), (GD, [(S, 0)], [])], [1.0, 0.0])
+        check("2mm-gated", [GB, GD, GE])
+        if h.stats()["gated_products"] - g0 != 3:  # B once, D twice (this rank's device)
+            bad.append(("gated", h.stats()["gated_products"] - g0))
         # Reduce over NVLink sync words: every rank gets the oracle's value
         ints = np.arange(np.prod(shape), dtype=np.float64).reshape(shape) % 97
         for be in (h, w):

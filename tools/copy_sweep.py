@@ -3,7 +3,7 @@ practical ceiling for a per-GPU stencil share of that size.  Not part of the lib
 import torch
 
 torch.cuda.init()
-for mb in (16, 32, 64, 128, 256, 512, 1024):
+for mb in (16, 32, 64, 128, 256, 512, 1024, 2048, 4096):
     n = mb * (1 << 20) // 8
     a = torch.empty(n, dtype=torch.float64, device="cuda")
     b = torch.empty_like(a)
