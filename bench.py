@@ -52,6 +52,15 @@ def dist_env():
     return ws, rank, local
 
 
+def _env_int(name, default):
+    """The library's kernel switches (read once per process by libhdarray), for naming
+    the kernel a roofline line describes."""
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -192,7 +201,8 @@ class Stencil:
             self.K, self.uses, self.part_kind = H.K_JACOBI5, J, H.ROW
             self.modes = (37, 61)
             self.workload = jacobi_workload(self.n)
-            self.kname = "stencil2d_kernel<double,JACOBI5>"
+            self.kname = ("stencil2d_tma_kernel<double,0> (TMA ring)" if _env_int("HDA_TMA", 0) == 2
+                          else "stencil2d_kernel<double,JACOBI5>")
         elif kind == "stencil9":
             self.n = n or 16384
             self.shape, self.dt, self.es = (self.n, self.n), H.F64, 8
@@ -200,7 +210,8 @@ class Stencil:
             self.modes = (3, 4)
             self.workload = (f"configs[2]: {self.n}x{self.n} fp64 9-point stencil (R12), BLOCK partition of the "
                              "interior with corner halos, ping-pong sweeps")
-            self.kname = "stencil2d_kernel<double,STENCIL9>"
+            self.kname = ("stencil2d_tma_kernel<double,1> (TMA ring)" if _env_int("HDA_TMA", 0) >= 1
+                          else "stencil2d_kernel<double,STENCIL9>")
         else:
             self.n = n or 1024
             self.shape, self.dt, self.es = (self.n,) * 3, H.F32, 4
@@ -358,7 +369,8 @@ class Gemm:
         self.acc = [(self.C, [], [(0, 0)]), (self.A, [(0, S)], []), (self.B, [(S, 0)], [])]
         self.kind = "gemm"
         self.workload = f"configs[4] (product half): {n}^2 bf16 GEMM, fp32 accumulate and C, ROW partition, B use=all"
-        self.kname = "gemm2_kernel<float> (tcgen05 cta_group::2)"
+        self.kname = ("gemm2_kernel<float> (tcgen05 cta_group::2)" if _env_int("HDA_GEMM_2SM", 1)
+                      else "gemm_kernel<float> (tcgen05)")
         self.dtype_name = "bf16"
         self.metric_unit = "TFLOP/s"
         self.bound = "tensor"
@@ -426,7 +438,8 @@ class TwoMM:
         self.kind = "2mm"
         self.workload = (f"SURVEY 8(f)-1 2MM chain (P:L425): D=AxB, E=CxD, {n}^2 bf16 in, D bf16, E fp32, "
                          f"{part.upper()} partition")
-        self.kname = "gemm_kernel (tcgen05), two launches per step"
+        self.kname = ("gemm2_kernel (tcgen05 cta_group::2), two launches per step" if _env_int("HDA_GEMM_2SM", 1)
+                      else "gemm_kernel (tcgen05), two launches per step")
         self.dtype_name = "bf16"
         self.metric_unit = "TFLOP/s"
         self.flops_per_step = 4.0 * n ** 3

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <utility>
 
+#include "divc.cuh"
 #include "kernels.cuh"
 #include "sync.cuh"
 
@@ -338,7 +339,7 @@ __device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
   T c = ((nw + ne) + sw) + se;
   T t = T(4) * a;
   t = t + c;
-  return t / T(20);
+  return div20(t);
 }
 
 // KIND 0 = JACOBI5, 1 = STENCIL9

@@ -16,11 +16,11 @@
 // STENCIL9 e=((W+E)+N)+S, c=((NW+NE)+SW)+SE, (4e+c)/20 — results are bit-identical
 // to the register-march kernels in kernels.cu and to the oracle.
 //
-// Measured (tools/stencil_tma_tune.cu, profiles/r02/stencil_tma/): the 9-point kernel
-// is latency/issue-bound on its IEEE fp64 division in the register-march design; here
-// the loads are decoupled from the math and it runs 12-20% faster; for the 5-point
-// Jacobi the register-march kernel stays ahead and remains the default (HDA_TMA=2 uses
-// this kernel for both).
+// Measured (tools/stencil_tma_tune.cu): with nvcc's IEEE fp64 division (the reciprocal
+// of 20 rebuilt per point) the register-march 9-point kernel was latency-bound and this
+// one ran up to 12-20% faster standalone; once the division uses a constant reciprocal
+// (divc.cuh) the register march is ahead (0.873 vs 0.78 of HBM at N=1), so this kernel
+// is opt-in: HDA_TMA=1 (9-point), 2 (both).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -31,6 +31,7 @@
 #include <mutex>
 #include <unordered_map>
 
+#include "divc.cuh"
 #include "kernels.cuh"
 #include "sync.cuh"
 #include "tcgen05_common.cuh"
@@ -94,7 +95,7 @@ __device__ __forceinline__ T st9(T w, T e, T n, T s, T nw, T ne, T sw, T se) {
   T c = ((nw + ne) + sw) + se;
   T t = T(4) * a;
   t = t + c;
-  return t / T(20);
+  return div20(t);
 }
 
 template <typename T, int KIND>
@@ -303,11 +304,14 @@ static cudaError_t launch_t(const T* in, T* out, const int64_t* shape, const int
 
 }  // namespace stma
 
-// HDA_TMA: 1 (default) = TMA ring for the 9-point kernel, 0 = off, 2 = 9-point and Jacobi
+// HDA_TMA: 0 (default) = off, 1 = TMA ring for the 9-point kernel, 2 = 9-point and
+// Jacobi.  With the constant-reciprocal division (divc.cuh) the register march is ahead
+// for the 9-point too: 357.5-357.7 vs 320.2-320.9 GPoints/s at N=1, 691.9 vs 629.6-632.7
+// at N=2 (profiles/r02/div20/)
 int stencil_tma_mode() {
   static const int v = [] {
     const char* e = std::getenv("HDA_TMA");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }

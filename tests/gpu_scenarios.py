@@ -121,16 +121,20 @@ def tma_shapes(G):
     """TMA-ring 2-D stencils (stencil_tma.cu) on boxes spanning several 252/248-column
     strips and several row blocks, with ragged ends, boxes that start off the 32-byte
     strip alignment and partitions whose devices get different tile heights; every
-    replica against the oracle, bit for bit, f64 and f32, 5- and 9-point."""
+    replica against the oracle, bit for bit, f64 and f32, 5- and 9-point, uniform and
+    special-value inputs."""
     J = [(0, -1), (0, 1), (-1, 0), (1, 0)]
     N9 = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1) if i or j]
     bad = []
     cases = [((517, 1111), 1, (1, 1), None), ((300, 1500), 2, (5, 7), (291, 1433)), ((1000, 600), 3, (1, 3), None),
              ((133, 2050), 1, (40, 250), (100, 1900))]
     for dt, name in ((H.F64, "f64"), (H.F32, "f32")):
-        for shape, P, lb, ub in cases:
+        # the first shape also with Inf / signed zeros / subnormals / huge values mixed in
+        # (the divisions' slow paths inside the TMA consumers)
+        for ci, (shape, P, lb, ub, u0) in enumerate(
+                [(c[0], c[1], c[2], c[3], synth.uniform(31, c[0], name)) for c in cases] +
+                [(cases[0][0], 2, cases[0][2], None, synth.special_values(32, cases[0][0], name))]):
             ub = ub or (shape[0] - 1, shape[1] - 1)
-            u0 = synth.uniform(31, shape, name)
             for K, uses in ((H.K_JACOBI5, J), (H.K_STENCIL9, N9)):
                 h = H.HDArray(n_gpus=G, n_devices=P)
                 w = O.Oracle(P)

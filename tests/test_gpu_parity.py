@@ -7,6 +7,8 @@ both sides use the same operand order and IEEE operations); the product within
 1e-2 relative Frobenius (integer cases bit-exact).  Every replica of every device is
 compared, so out-of-region writes and stale halos are caught.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -166,9 +168,9 @@ def test_stencil7_3d_bit_exact(H, dtype):
 def test_stencil_division_edge_values(H, dtype):
     """Stencils on fields with +Inf, signed zeros, subnormals, tiny and huge normals
     mixed into uniform data (the divisions by 20 and 6 on their slow paths, Inf
-    propagation, sign of zero): every replica bit-identical to the oracle.  2-D boxes
-    large enough for the TMA kernel (ROW) and small enough for the register march (COL,
-    4 devices)."""
+    propagation, sign of zero): every replica bit-identical to the oracle, on the
+    default kernels (the TMA-ring ones: test_stencil2d_tma_shapes).  2-D boxes with
+    full 16-row tiles (ROW) and thin strips (COL, 4 devices)."""
     DT = H.F64 if dtype == "f64" else H.F32
     cases = [((90, 420), "ROW", 2, H.K_STENCIL9, N9), ((37, 53), "COL", 4, H.K_STENCIL9, N9),
              ((20, 26, 140), "ROW", 2, H.K_STENCIL7_3D, N7)]
@@ -185,6 +187,22 @@ def test_stencil_division_edge_values(H, dtype):
                 be.apply(K, part, [(dst, [], [(0,) * len(shape)]), (src, uses, [])])
         assert_replicas(h, w, [X, Y], P)
         h.close()
+
+
+def test_div20_matches_ieee(tmp_path):
+    """The 9-point stencil's fp64 division (csrc/divc.cuh: Markstein correction with a
+    constant reciprocal on [2^-1000, 2^1000], the IEEE division elsewhere) is bit-
+    identical to a / 20.0 on 2^32 inputs covering every exponent, both range edges,
+    zeros, subnormals, Inf and NaN (tools/div20_check.cu, built here with nvcc)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "div20_check")
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-I",
+                    os.path.join(root, "paper_1809_05657_b200", "csrc"), os.path.join(root, "tools", "div20_check.cu"),
+                    "-o", exe], check=True, timeout=300)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 mismatches" in r.stdout
 
 
 # ------------------------------------------------------------------ repartition
