@@ -29,4 +29,19 @@ __device__ __forceinline__ double div20(double a) {
 // fp32: nvcc already folds 1/20 into a constant (FFMA correction + FCHK); keep it
 __device__ __forceinline__ float div20(float a) { return a / 20.0f; }
 
+// The 3-D 7-point stencil's fp32 division by 6 (reading R13), same scheme: y = RN(1/6);
+// no reciprocal refinement and no FCHK on the fast path.  Exhaustively checked against
+// a / 6.0f on all 2^32 inputs (tools/div20_check.cu).
+__device__ __forceinline__ float div6(float a) {
+  const float y = 0x1.555556p-3f;  // RN(1/6)
+  const float m = fabsf(a);
+  if (m >= 0x1p-100f && m <= 0x1p+100f) {
+    const float q0 = __fmul_rn(a, y);
+    const float r = __fmaf_rn(-q0, 6.0f, a);
+    return __fmaf_rn(r, y, q0);
+  }
+  return a / 6.0f;
+}
+__device__ __forceinline__ double div6(double a) { return a / 6.0; }
+
 }  // namespace hda

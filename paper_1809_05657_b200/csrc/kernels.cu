@@ -316,6 +316,14 @@ static int tail_rows() {
   static const int v = env_or("HDA_TAIL_ROWS", 4);
   return v;
 }
+// HDA_ST_PF (5-point) / HDA_ST9_PF (9-point): L2 bulk-prefetch distance of the 2-D
+// register-march stencils, in row groups (0 = off).  Measured on one B200 (N=1,
+// profiles/r02/prefetch/): Jacobi 8192^2 0.897 -> 0.970 of HBM at 1 (0.957 at 2);
+// 9-point 16384^2 0.795 -> 0.917 at 1 (0.891 at 2, 0.875 at 3)
+static int st_prefetch(int kind) {
+  static const int p5 = env_or("HDA_ST_PF", 1), p9 = env_or("HDA_ST9_PF", 1);
+  return kind == 0 ? p5 : p9;
+}
 static int tail_waves() {
   static const int v = env_or("HDA_TAIL_WAVES", 1);
   return v;
@@ -352,12 +360,13 @@ struct Boxes2 {
   int32_t gx[8], gy[8];
   int32_t n;
   int32_t ndep_first;  // fused halo kernel: boxes [0, ndep_first) are the boundary strips
+  int32_t pf;          // L2 bulk prefetch distance in row groups (HDA_ST_PF; 0 = off)
 };
 
 template <typename T, int KIND, int ROWS, bool CG>
 __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __restrict__ out, int64_t ld,
                                                int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t cbase,
-                                               int64_t rpb, int64_t xb, int64_t yb) {
+                                               int64_t rpb, int64_t xb, int64_t yb, int pf = 0) {
   constexpr int V = V16<T>::n;
   constexpr int W = ST_GROUP + 2;
   const int lane = threadIdx.x & 31;
@@ -387,9 +396,25 @@ __device__ __forceinline__ void stencil2d_body(const T* __restrict__ in, T* __re
     if (lane == 31 && live && col + V < ld) R = CG ? __ldcg(in + row * ld + col + V) : __ldg(in + row * ld + col + V);
   };
 
+  // L2 bulk prefetch pf row groups ahead: lane 0 of warp k < ST_GROUP prefetches the
+  // block's span of one row, so the demand loads meet L2 rather than DRAM latency
+  const int wid = threadIdx.x >> 5;
+  const int64_t col0 = cbase + xb * ST_THREADS * V;
+  const uint32_t span = (uint32_t)(min((int64_t)ST_THREADS * V, ld - col0) * (int64_t)sizeof(T));
+  const bool pf_on = pf > 0 && lane == 0 && col0 < ld && (ld * (int64_t)sizeof(T)) % 16 == 0;
+  auto prefetch_row = [&](int64_t row) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(in + row * ld + col0), "r"(span) : "memory");
+  };
+  if (pf_on)
+    for (int64_t row = rs + 1 + wid; row <= min(re, rs + (int64_t)ST_GROUP * pf); row += ST_THREADS / 32)
+      prefetch_row(row);
   load_row(w[0], rs - 1);
   load_row(w[1], rs);
   for (int64_t base = rs; base < re; base += ST_GROUP) {
+    if (pf_on && wid < ST_GROUP) {
+      const int64_t row = base + 1 + (int64_t)ST_GROUP * pf + wid;
+      if (row <= re) prefetch_row(row);
+    }
 #pragma unroll
     for (int k = 0; k < ST_GROUP; k++)
       if (base + 1 + k <= re) load_row(w[k + 2], base + 1 + k);
@@ -464,7 +489,7 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
     int64_t xb, yb;
     tile_of(bx, blockIdx.x, b, xb, yb);
     stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                         bx.rpb[b], xb, yb);
+                                         bx.rpb[b], xb, yb, bx.pf);
   }
   ks_post(ks);
 }
@@ -569,7 +594,7 @@ __global__ void __launch_bounds__(ST_THREADS, KIND == 0 ? HALO_MINB0 : ST_MINB)
     }
   } else {
     stencil2d_body<T, KIND, ROWS, false>(in, out, ld, bx.r0[b], bx.r1[b], bx.c0[b], bx.c1[b], bx.cbase[b],
-                                         bx.rpb[b], xb, yb);
+                                         bx.rpb[b], xb, yb, bx.pf);
   }
   ks_post(ks);
 }
@@ -610,6 +635,7 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     Boxes2 bx;
     bx.n = 0;
     bx.ndep_first = 0;
+    bx.pf = st_prefetch(KIND);
     for (int i = 0; i < nb && bx.n < 8; i++) {
       const int64_t r0 = lbs[i][1], r1 = ubs[i][1], c0 = lbs[i][2], c1 = ubs[i][2];
       if (r0 >= r1 || c0 >= c1 || lbs[i][0] >= ubs[i][0]) continue;
@@ -793,6 +819,7 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
   }
   bx.ndep_first = 0;
+  bx.pf = st_prefetch(KIND);
   if (dep_first && ni < bx.n) {  // rotate the boundary boxes to the front
     Boxes2 o = bx;
     int j = 0;
@@ -867,7 +894,7 @@ template <typename T>
 __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n1,
                                                          int64_t n2, int64_t z0, int64_t z1, int64_t y0, int64_t y1,
                                                          int64_t x0, int64_t x1, int64_t xbase, int64_t nbig,
-                                                         int64_t zt, const __grid_constant__ KSync ks) {
+                                                         int64_t zt, int pf, const __grid_constant__ KSync ks) {
   pdl_enter();
   ks_pre(ks);
   constexpr int V = V16<T>::n;
@@ -895,7 +922,21 @@ __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ 
     ld(zm[r], zs - 1, ya + r);
     ld(zc[r], zs, ya + r);
   }
+  // L2 prefetch pf planes ahead (HDA_S7_PF): warp w < S3_R + 2 bulk-prefetches its
+  // block's span of row ya - 1 + w, so the demand loads below meet L2, not DRAM latency
+  const int wid = threadIdx.x >> 5;
+  const int64_t span = min((int64_t)256 * V, n2 - (xbase + (int64_t)blockIdx.x * 256 * V));
+  const T* pfrow = in + (ya - 1 + wid) * n2 + xbase + (int64_t)blockIdx.x * 256 * V;
+  const bool pf_on = pf > 0 && lane == 0 && wid < S3_R + 2 && ya - 1 + wid < n1 && span > 0;
+  if (pf_on)
+    for (int d = 1; d < pf; d++)
+      if (zs + d < z1 + 1)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pfrow + (zs + d) * pl),
+                     "r"((uint32_t)(span * sizeof(T))) : "memory");
   for (int64_t z = zs; z < ze; z++) {
+    if (pf_on && z + pf < z1 + 1)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pfrow + (z + pf) * pl),
+                   "r"((uint32_t)(span * sizeof(T))) : "memory");
     T top[V], bot[V];
     ld(top, z, ya - 1);
     ld(bot, z, ya + S3_R);
@@ -922,7 +963,7 @@ __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ 
         s = s + yp[v];
         s = s + zm[r][v];
         s = s + zp[r][v];
-        o[v] = s / T(6);
+        o[v] = div6(s);
       }
       if (live && y < y1) {
         T* dst = out + z * pl + y * n2 + x;
@@ -962,7 +1003,7 @@ __global__ void stencil7_scalar_kernel(const T* __restrict__ in, T* __restrict__
     s = s + p[n2];
     s = s + p[-pl];
     s = s + p[pl];
-    out[z * pl + y * n2 + x] = s / T(6);
+    out[z * pl + y * n2 + x] = div6(s);
   }
   ks_post(ks);
 }
@@ -997,8 +1038,11 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
       ntail = (rest + zt - 1) / zt;
     }
     dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)(nbig + ntail));
+    // 1024^3 f32 (profiles/r02/prefetch/): 0.822 (off) -> 0.886 (1) -> 0.928-0.954 (2)
+    // -> 0.91 (3) -> 0.83-0.88 (4) -> 0.74 (6) of HBM
+    static const int pf = env_or("HDA_S7_PF", 2);
     cudaError_t e = launch_pdl(stencil7_kernel<T>, grid, dim3(256), s, in, out, n1, n2, lb[0], ub[0], lb[1], ub[1],
-                               lb[2], ub[2], xbase, nbig, zt, ks);
+                               lb[2], ub[2], xbase, nbig, zt, pf, ks);
     if (e != cudaSuccess) return e;
   } else {
     dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));

@@ -1,7 +1,8 @@
 // div20_check.cu — hda::div20 (csrc/divc.cuh, the 9-point stencil's fp64 division by
 // 20) against the IEEE division a / 20.0 on 2^32 hashed doubles: every exponent from
-// subnormal to huge, both signs, plus zeros, Inf, NaN and the range edges.  Prints the
-// mismatch count; exit 1 on any.  Run by tests/test_gpu_parity.py::test_div20_matches_ieee.
+// subnormal to huge, both signs, plus zeros, Inf, NaN and the range edges; and
+// hda::div6 (the 3-D stencil's fp32 division by 6) against a / 6.0f on every one of the
+// 2^32 fp32 bit patterns.  Prints the mismatch counts; exit 1 on any.  Run by tests/test_gpu_parity.py::test_div20_matches_ieee.
 #include <cstdio>
 #include <cstdint>
 
@@ -37,6 +38,16 @@ __global__ void check(uint64_t n, unsigned long long* bad, unsigned long long* f
   }
 }
 
+__global__ void check6(unsigned long long* bad, unsigned long long* first) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (1ull << 32);
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float a = __uint_as_float((unsigned)i);
+    const float g = hda::div6(a), w = a / 6.0f;
+    const bool same = __float_as_uint(g) == __float_as_uint(w) || (g != g && w != w);
+    if (!same && atomicAdd(bad, 1ull) == 0) *first = i;
+  }
+}
+
 int main() {
   unsigned long long *bad, *first;
   cudaMallocManaged(&bad, 8);
@@ -52,5 +63,15 @@ int main() {
   printf("div20 vs IEEE: %llu mismatches in %llu inputs", *bad, (unsigned long long)n);
   if (*bad) printf(" (first input bits %016llx)", *first);
   printf("\n");
-  return *bad ? 1 : 0;
+  const unsigned long long bad20 = *bad;
+  *bad = 0;
+  check6<<<148 * 8, 256>>>(bad, first);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    printf("CUDA error\n");
+    return 2;
+  }
+  printf("div6 (fp32) vs IEEE: %llu mismatches in all 4294967296 inputs", *bad);
+  if (*bad) printf(" (first input bits %08llx)", *first);
+  printf("\n");
+  return (bad20 || *bad) ? 1 : 0;
 }
