@@ -887,14 +887,21 @@ cudaError_t launch_stencil9(int dtype, const void* in, void* out, const int64_t*
 // keeping planes z-1, z, z+1 in registers.  Tuned on 1024^3 f32: 84% of HBM.
 // =====================================================================================
 
-constexpr int S3_R = 2;     // y rows per thread
-constexpr int S3_ZCH = 32;  // planes per block
+#ifndef S3_R_DEF
+#define S3_R_DEF 2
+#endif
+#ifndef S3_ZCH_DEF
+#define S3_ZCH_DEF 32
+#endif
+constexpr int S3_R = S3_R_DEF;      // y rows per thread
+constexpr int S3_ZCH = S3_ZCH_DEF;  // planes per block
 
 template <typename T>
 __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t n1,
                                                          int64_t n2, int64_t z0, int64_t z1, int64_t y0, int64_t y1,
                                                          int64_t x0, int64_t x1, int64_t xbase, int64_t nbig,
-                                                         int64_t zt, int pf, const __grid_constant__ KSync ks) {
+                                                         int64_t zt, int pf, int pf_halo,
+                                                         const __grid_constant__ KSync ks) {
   pdl_enter();
   ks_pre(ks);
   constexpr int V = V16<T>::n;
@@ -922,12 +929,15 @@ __global__ void __launch_bounds__(256, 4) stencil7_kernel(const T* __restrict__ 
     ld(zm[r], zs - 1, ya + r);
     ld(zc[r], zs, ya + r);
   }
-  // L2 prefetch pf planes ahead (HDA_S7_PF): warp w < S3_R + 2 bulk-prefetches its
-  // block's span of row ya - 1 + w, so the demand loads below meet L2, not DRAM latency
+  // L2 prefetch pf planes ahead (HDA_S7_PF): warp w < S3_R bulk-prefetches its block's
+  // span of row ya + w (with HDA_S7_PF_HALO=1 also the rows above and below, which
+  // other blocks prefetch too), so the demand loads below meet L2, not DRAM latency
   const int wid = threadIdx.x >> 5;
   const int64_t span = min((int64_t)256 * V, n2 - (xbase + (int64_t)blockIdx.x * 256 * V));
-  const T* pfrow = in + (ya - 1 + wid) * n2 + xbase + (int64_t)blockIdx.x * 256 * V;
-  const bool pf_on = pf > 0 && lane == 0 && wid < S3_R + 2 && ya - 1 + wid < n1 && span > 0;
+  const int halo = pf_halo ? 1 : 0;
+  const int64_t pr = ya - halo + wid;
+  const T* pfrow = in + pr * n2 + xbase + (int64_t)blockIdx.x * 256 * V;
+  const bool pf_on = pf > 0 && lane == 0 && wid < S3_R + 2 * halo && pr < n1 && span > 0;
   if (pf_on)
     for (int d = 1; d < pf; d++)
       if (zs + d < z1 + 1)
@@ -1038,11 +1048,12 @@ static cudaError_t launch_stencil7_t(const T* in, T* out, const int64_t* shape, 
       ntail = (rest + zt - 1) / zt;
     }
     dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)(nbig + ntail));
-    // 1024^3 f32 (profiles/r02/prefetch/): 0.822 (off) -> 0.886 (1) -> 0.928-0.954 (2)
-    // -> 0.91 (3) -> 0.83-0.88 (4) -> 0.74 (6) of HBM
-    static const int pf = env_or("HDA_S7_PF", 2);
+    // 1024^3 f32, 30 steps (profiles/r02/prefetch/): 0.822 (off) -> 0.886 (1) ->
+    // 0.928-0.954 (2) -> 0.91 (3) -> 0.83-0.88 (4) -> 0.74 (6) of HBM with the halo
+    // rows; 100 steps (power-capped): own rows 0.858-0.866 vs 0.826-0.832 with halos
+    static const int pf = env_or("HDA_S7_PF", 2), pf_halo = env_or("HDA_S7_PF_HALO", 0);
     cudaError_t e = launch_pdl(stencil7_kernel<T>, grid, dim3(256), s, in, out, n1, n2, lb[0], ub[0], lb[1], ub[1],
-                               lb[2], ub[2], xbase, nbig, zt, pf, ks);
+                               lb[2], ub[2], xbase, nbig, zt, pf, pf_halo, ks);
     if (e != cudaSuccess) return e;
   } else {
     dim3 grid((unsigned)((ub[2] - lb[2] + 127) / 128), (unsigned)(ub[1] - lb[1]), (unsigned)(ub[0] - lb[0]));
