@@ -606,6 +606,11 @@ def main():
             if ws > 1:
                 torch.cuda.synchronize()
                 dist.barrier()
+            # ~100 us of device sleep before the start event: the host issues the step
+            # (tens of us) while the GPU sleeps, so the event pair brackets the device's
+            # step as in the back-to-back mode, not the host's issue latency after an idle
+            with torch.cuda.stream(stream):
+                torch.cuda._sleep(200000)
             evs[i][0].record(stream)
             wl.step()
             evs[i][1].record(stream)
@@ -781,7 +786,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": wl.dtype_name, "data": "synthetic",
             "config": {"workload": wl.workload, "n": wl.n, "parallelism": f"spmd{ws}" if ws > 1 else "single",
                        "transport": ["fused", "staged", "auto"][args.transport], "overlap": not args.no_overlap,
-                       "l2": ("L2 flushed between timed steps (write a 2x-L2 buffer, then read another)" if flush else
+                       "l2": ("L2 flushed between timed steps (write a 2x-L2 buffer, then read another; each step is "
+                              "queued behind a 100 us device sleep so its events bracket device time)" if flush else
                               f"inputs larger than L2 (per-GPU working set {wl.working_set / 2**20:.0f} MiB)")},
             **({"note": "one device: a repartition moves nothing (value 0); the roofline is the SCALE kernel's"}
                if args.workload == "repartition" and ws == 1 else {}),

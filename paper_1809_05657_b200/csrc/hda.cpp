@@ -1388,9 +1388,14 @@ static int issue_kernel(hda_ctx_t* ctx, const Transition* t, unsigned long long 
   // user kernels publish PROD from a trailing signal launch (HDA_SIG_KERNEL=0: from
   // the kernel's last CTA, after a fence in every CTA)
   static const int sig_kernel = env_int("HDA_SIG_KERNEL", 1);
+  // the fused halo launch (one kernel per step) keeps its signal in its last CTA: one
+  // launch instead of two per step, measured on 4 B200s with 134 MB shares (N=8-sized,
+  // 5792^2): 962-968 vs 942-943 GPoints/s (HDA_HALO_SIG_TRAIL=1 restores the trailing
+  // launch; profiles/r02/halo_sig/)
+  static const int halo_sig_trail = env_int("HDA_HALO_SIG_TRAIL", 0);
   SignalList post_sig;
   post_sig.n = 0;
-  const bool split_sig = sig_kernel && kern && !io && ks.nsig > 0;
+  const bool split_sig = sig_kernel && kern && !io && ks.nsig > 0 && (halo_sig_trail || !ctx->halo_job[q]);
   if (split_sig) {
     for (int i = 0; i < ks.nsig; i++) post_sig.ptr[i] = ks.sig_ptr[i];
     post_sig.n = ks.nsig;
