@@ -333,6 +333,12 @@ constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
 constexpr int ST_ROWS = 16;      // rows per block
 constexpr int ST_MINB = 4;       // resident blocks per SM (register cap)
+#ifndef ST9_MINB
+// the 9-point kernel's register cap (blocks per SM): 5 spilled (48 registers); with the
+// constant-reciprocal division and the L2 prefetch, 4 (64 registers, no spills) is ahead:
+// 376 vs 364 GPoints/s at 40 sweeps, 344 vs 330 at 200 (profiles/r02/stencil9_minb/)
+#define ST9_MINB 4
+#endif
 
 template <typename T>
 __device__ __forceinline__ T quarter(T x);
@@ -479,7 +485,7 @@ __device__ __forceinline__ void tile_of(const Boxes2& bx, int64_t t, int& b, int
 }
 
 template <typename T, int KIND, int ROWS>
-__global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST_MINB + 1 : ST_MINB)
+__global__ void __launch_bounds__(ST_THREADS, KIND == 1 ? ST9_MINB : ST_MINB)
     stencil2d_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t ld, const __grid_constant__ Boxes2 bx,
                      const __grid_constant__ KSync ks) {
   pdl_enter();
