@@ -958,13 +958,32 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
       count_launch(ctx);
     }
   }
+  // Comm-stream SM pull: wait in one CTA, then launch the copy with no waits.  Folded
+  // into the pull kernel, every one of its CTAs would spin on the writers' PROD words for
+  // as long as the neighbours take to finish their previous step (~30 us at N=4), holding
+  // SM slots the interior launch running beside it needs (HDA_PULL_WAIT_KERNEL=0: fold)
+  static const int pull_wait_kernel = env_int("HDA_PULL_WAIT_KERNEL", 1);
+  bool waited_outside = false;
+  if (nb > 0 && comm && pull_wait_kernel && pre.nwait > 0) {
+    KSync w = ks_empty(ctx);
+    std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
+    std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
+    w.nwait = pre.nwait;
+    w.delay_ns = pull_delay_ns(q);
+    RunBatch empty;
+    std::memset(&empty, 0, sizeof empty);
+    CK(launch_copy_runs(empty, w, st));
+    count_launch(ctx);
+    pre.nwait = 0;
+    waited_outside = true;
+  }
   for (size_t i = 0; i < nb; i++) {
     KSync ks = ks_empty(ctx);
     if (i == 0) {
       std::memcpy(ks.wait_ptr, pre.wait_ptr, sizeof ks.wait_ptr);
       std::memcpy(ks.wait_val, pre.wait_val, sizeof ks.wait_val);
       ks.nwait = pre.nwait;
-      ks.delay_ns = pull_delay_ns(q);
+      ks.delay_ns = waited_outside ? 0 : pull_delay_ns(q);
     }
     if (i + 1 == nb) {
       std::memcpy(ks.sig_ptr, post.sig_ptr, sizeof ks.sig_ptr);
