@@ -273,7 +273,7 @@ cudaError_t launch_gemm(int c_dtype, const void* A, const void* B, void* C, int6
                         cudaStream_t s, const KGate* gate) {
   const int64_t m0 = lb[1], m1 = ub[1], n0 = lb[2], n1 = ub[2];
   if (m0 >= m1 || n0 >= n1) return cudaSuccess;
-  const bool gated = gate && gate->n > 0;
+  const bool gated = gate && (gate->n > 0 || gate->nseg > 0);  // flags or K ranges: CTA-pair kernel only
   // CTA-pair kernel (gemm_tcgen05_2sm.cu) by default: 16384^2 back-to-back 1655-1691
   // vs 1462-1482 TFLOP/s for this single-CTA kernel (HDA_GEMM_2SM=0 selects it)
   static const int two_sm = [] {

@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int acc = 0;
       uint32_t aph = 0;
       for (int pp = 0; pp < npass && !aborted(); pp++) {
-        const int nkb = multi ? gate.skb1[pp] - gate.skb0[pp] : kblocks;
+        int nkb = 0;  // k-blocks per tile in this pass (all segments when one pass walks them)
+        for (int sg = multi ? pp : 0; sg < (multi ? pp + 1 : gate.nseg); sg++) nkb += gate.skb1[sg] - gate.skb0[sg];
         for (int64_t t = cid; t < n_tiles && !aborted(); t += ncl) {
           mbar_wait<true>(&tempty[acc], aph ^ 1);  // arrivals from both CTAs' epilogues
           fence_after();
@@ -420,6 +421,13 @@ cudaError_t launch_gemm_2sm(int c_dtype, const void* A, const void* B, void* C, 
       return e ? std::atoi(e) : 1;
     }();
     g.multi = (multi && c_dtype == 1 && ns > 1) ? 1 : 0;
+  } else if (gate && gate->nseg > 0) {
+    // explicit K ranges, no arrival flags (the two-launch split of a gated product)
+    if (gate->nseg > kMaxGate + 1) return cudaErrorNotSupported;
+    g = *gate;
+    g.n = 0;
+    for (int j = 0; j < g.nseg; j++)
+      if (g.skb0[j] < 0 || g.skb1[j] > kblocks || g.skb0[j] >= g.skb1[j]) return cudaErrorInvalidValue;
   } else {
     // measurement hook: HDA_DEBUG_GEMM_SEGS=s splits an ungated K into s passes (fp32 C)
     static const int dbg = [] {

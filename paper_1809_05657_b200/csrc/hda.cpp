@@ -830,17 +830,20 @@ static const MemOps& memops() {
     if (cr_ != CUDA_SUCCESS) return fail(ctx, HDA_ECUDA, "stream memory op failed: " #call); \
   } while (0)
 
-// HDA_GEMM_GATE (default 0, opt-in): a GEMM whose B rows arrive from other GPUs runs
-// gated on their arrival (all-gather overlapped with the product) instead of after a
-// join.  Measured slower on B200 (2MM ROW 16384^2 at N=2: 5.62-5.70 ms per step gated vs
-// 5.40 joined): the 256 MiB copy takes 0.43 ms either way, but the gated
-// product runs 0.68 ms longer.  Two passes cost 0.1-0.25 ms on their own (the second
-// re-reads and re-writes the fp32 C; HDA_DEBUG_GEMM_SEGS), a concurrent copy slows a
-// product by 0-0.17 ms (tools/ce_contention.py); the rest is not accounted for.
-static bool gate_enabled() {
-  static const int v = env_int("HDA_GEMM_GATE", 0);
-  return v != 0;
+// HDA_GEMM_GATE: how a GEMM whose B rows arrive from other GPUs (copy-engine blocks,
+// arrival flags written by the comm stream) overlaps that all-gather.
+//   2 (default) split: with an fp32 C and whole k-blocks per source, one launch over the
+//     resident rows beside the copies, a second (C += ...) after them; otherwise joined.
+//     2MM ROW 16384^2: N=2 5.25-5.29 vs 5.51 ms per step joined, N=4 2.80 vs 3.09.
+//   1 gated inside the kernel: producers wait per k-block for the sources' flags (with
+//     fp32 C, K in per-segment passes).  Slower than joining (N=2: 5.62-5.70 vs 5.40):
+//     the copies take 0.43 ms either way, the gated product 0.68 ms longer.
+//   0 joined: copies, then the product.
+static int gate_mode() {
+  static const int v = env_int("HDA_GEMM_GATE", 2);
+  return v;
 }
+static bool gate_enabled() { return gate_mode() != 0; }
 
 // The gated product's exchange (reader q): on the comm stream, forked after everything
 // issued before this call, per source in the permutation order (q+1, q+2, ...): wait for
@@ -1256,6 +1259,49 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
     case KN_GEMM: {
       const TArray& A = ctx->tr->array(ci.param_array[1]);
       const TArray& B = ctx->tr->array(ci.param_array[2]);
+      const int64_t K = A.shape[1];
+      // HDA_GEMM_GATE=2, split form: with an fp32 C and whole k-blocks per source, the
+      // resident rows' product runs as one launch beside the copies and the arrived rows'
+      // product as a second launch after them (C += ...), no in-kernel gating
+      constexpr int64_t BK = 64;  // the CTA-pair GEMM's k-block
+      if (gate && gate->n > 0 && gate_mode() == 2 && a0.dtype == HDA_F32) {
+        const int64_t kb = (K + BK - 1) / BK;
+        std::vector<char> remote(kb, 0);
+        bool aligned = true;
+        for (int i = 0; i < gate->n; i++) {
+          if (gate->lo[i] % BK || (gate->hi[i] % BK && gate->hi[i] != K)) aligned = false;
+          for (int64_t b = gate->lo[i] / BK; b * BK < gate->hi[i] && b < kb; b++) remote[b] = 1;
+        }
+        int64_t a = 0;
+        while (a < kb && remote[a]) a++;
+        int64_t b = a;
+        while (b < kb && !remote[b]) b++;
+        bool contiguous = a < b;
+        for (int64_t x = b; x < kb; x++) contiguous &= remote[x] != 0;
+        KGate g1, g2;
+        std::memset(&g1, 0, sizeof g1);
+        std::memset(&g2, 0, sizeof g2);
+        g1.nseg = 1, g1.skb0[0] = (int32_t)a, g1.skb1[0] = (int32_t)b;
+        if (a > 0) g2.skb0[g2.nseg] = 0, g2.skb1[g2.nseg++] = (int32_t)a;
+        if (b < kb) g2.skb0[g2.nseg] = (int32_t)b, g2.skb1[g2.nseg++] = (int32_t)kb;
+        if (aligned && contiguous && g2.nseg > 0) {
+          cudaError_t e = launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
+                                      (float)scalars[0], (float)scalars[1], ks_part(ctx, ks, true, false), s, &g1);
+          if (e == cudaSuccess) {
+            count_launch(ctx);
+            CK(cudaStreamWaitEvent(s, ctx->gpus[ctx->dev[q].gpu].ev_pull, 0));
+            CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
+                           (float)scalars[0], 1.0f, ks_part(ctx, ks, false, true), s, &g2));
+            __atomic_fetch_add(&ctx->stats.gated_products, (int64_t)1, __ATOMIC_RELAXED);
+            break;
+          }
+          if (e != cudaErrorNotSupported) CK(e);
+        }
+      }
+      if (gate && gate_mode() == 2) {  // not splittable: join the copies first
+        CK(cudaStreamWaitEvent(s, ctx->gpus[ctx->dev[q].gpu].ev_pull, 0));
+        gate = nullptr;
+      }
       cudaError_t e = launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], A.shape[1], fb.lb, fb.ub,
                                   (float)scalars[0], (float)scalars[1], ks, s, gate);
       if (e == cudaSuccess && gate) __atomic_fetch_add(&ctx->stats.gated_products, (int64_t)1, __ATOMIC_RELAXED);

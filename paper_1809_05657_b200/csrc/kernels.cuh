@@ -133,7 +133,8 @@ cudaError_t launch_share(const unsigned long long* local, const SignalList& slot
 // exactly [0, K/64)), resident rows first, then the sources in arrival order.  multi:
 // one pass over all output tiles per segment, each pass adding its partial product to C
 // (fp32 C only), so the resident rows' work covers the first copies instead of every
-// tile stalling on its first remote k-block.  n == 0: no gating.
+// tile stalling on its first remote k-block.  n == 0 and nseg == 0: no gating, all of K;
+// n == 0 and nseg > 0: only the listed K ranges, in one pass, no flags (the split form).
 constexpr int kMaxGate = 16;
 struct KGate {
   int32_t n, nseg, multi, pad_;

@@ -156,8 +156,9 @@ def gemm_gate(G):
     on the copy engine, so the product runs gated on their arrival (KGate, own rows
     first) instead of after a join.  Integer bf16 inputs in [-1, 1]: D rounds to bf16
     the same way on both sides and |E| <= 2^20, so E (fp32) is exact in any k order and
-    every replica must equal the oracle's bit for bit.  HDA_GEMM_GATE=0 (the default)
-    runs the same program joined (the A/B).  Exits nonzero on a mismatch or when no product was gated
+    every replica must equal the oracle's bit for bit.  HDA_GEMM_GATE=2 (the default)
+    splits the fp32 products into a launch beside the copies and one after them, 1 gates
+    inside the kernel, 0 joins (the A/B).  Exits nonzero on a mismatch or when no product was gated
     though gating is on."""
     P, S = G, H.STAR
     bad, gated = [], 0
@@ -180,8 +181,10 @@ def gemm_gate(G):
         gated += h.stats()["gated_products"]
         h.close()
     # the gated kernel is the CTA-pair one (HDA_GEMM_2SM=0 selects the single-CTA kernel)
-    on = os.environ.get("HDA_GEMM_GATE", "0") != "0" and os.environ.get("HDA_GEMM_2SM", "1") != "0"
-    want = 2 * 4 * P if on else 0  # per size: B once, D three times, on every device
+    mode = os.environ.get("HDA_GEMM_GATE", "2") if os.environ.get("HDA_GEMM_2SM", "1") != "0" else "0"
+    # 1: per size B once and D three times on every device; 2 (split): only the fp32 E
+    # products with whole k-blocks per source (1024, not 1064), the bf16 D products join
+    want = {"0": 0, "1": 2 * 4 * P, "2": 3 * P}[mode]
     if gated != want:
         bad.append(f"gated products {gated}, expected {want}")
     print(f"gated products: {gated}")

@@ -662,12 +662,14 @@ def test_staged_plan_replay_after_regrow(G):
 
 
 @pytest.mark.parametrize("G", [2, 4])
-@pytest.mark.parametrize("gate", ["1", "0"])
+@pytest.mark.parametrize("gate", ["1", "2", "0"])
 def test_gemm_gated_allgather(G, gate):
     """The all-gather of B / D fused into the product (2MM ROW on G GPUs, 256 KiB copy
     threshold so 1024^2 blocks take the copy engine): bit-exact vs the oracle, gated
-    (HDA_GEMM_GATE=1, every incoming row block waited for per k-block inside the GEMM)
-    and joined (0)."""
+    (HDA_GEMM_GATE=1, every incoming row block waited for per k-block inside the GEMM),
+    split (2: fp32 C with whole k-blocks per source as two launches, resident rows
+    beside the copies and the arrived rows after them; the rest as in 1) and joined
+    (0)."""
     if ngpus() < G:
         pytest.skip(f"needs {G} GPUs")
     r = _scenario("gemm_gate", G, HDA_GEMM_GATE=gate, HDA_CE_BYTES="262144")

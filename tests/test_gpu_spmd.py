@@ -24,11 +24,11 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q, env1):
+def _worker(rank, world, port, q, env1, gate):
     try:
         os.environ["HDA_TIMEOUT_MS"] = "20000"  # a protocol deadlock fails in seconds
         os.environ["HDA_CE_BYTES"] = "262144"  # 2MM's 512 KiB row blocks on the copy engine (gated product)
-        os.environ["HDA_GEMM_GATE"] = "1"  # opt-in: the gated product is not the default
+        os.environ["HDA_GEMM_GATE"] = gate  # 1: gated inside the kernel; 2 (default): split launches
         if rank == 1:  # rank 1 only: an asymmetric slow reader opens the WAR window
             os.environ.update(env1)
         import torch
@@ -122,9 +122,10 @@ def _worker(rank, world, port, q, env1):
                 be.apply(H.K_GEMM, gp, [(GD, [], [(0, 0)]), (GA, [(0, S)], []), (GB, [(S, 0)], [])], [1.0, 0.0])
                 be.apply(H.K_GEMM, gp, [(GE, [], [(0, 0)]), (GC, [(0, S)], []), (GD, [(S, 0)], [])], [1.0, 0.0])
         check("2mm-gated", [GB, GD, GE])
-        # B once, D twice (this rank's device); at 8 ranks the 128-row shares are below the
-        # CTA-pair kernel's 256 rows, so the product joins the copies instead
-        if world <= 4 and h.stats()["gated_products"] - g0 != 3:
+        # gated: B once, D twice (this rank's device); split: the two fp32 E products only
+        # (the bf16 D products join); at 8 ranks the 128-row shares are below the
+        # CTA-pair kernel's 256 rows, so the products join the copies instead
+        if world <= 4 and h.stats()["gated_products"] - g0 != {"1": 3, "2": 2}[gate]:
             bad.append(("gated", h.stats()["gated_products"] - g0))
         # Reduce over NVLink sync words: every rank gets the oracle's value
         ints = np.arange(np.prod(shape), dtype=np.float64).reshape(shape) % 97
@@ -148,11 +149,11 @@ def _worker(rank, world, port, q, env1):
         q.put((rank, ["exception", traceback.format_exc()], 0, 0))
 
 
-def _run(world, env1):
+def _run(world, env1, gate="1"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, q, env1)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q, env1, gate)) for r in range(world)]
     for p in ps:
         p.start()
     out = [q.get(timeout=300) for _ in ps]
@@ -175,6 +176,16 @@ def test_spmd_two_gpus(env1):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, env1)
+
+
+def test_spmd_two_gpus_split_product():
+    """The default split product (HDA_GEMM_GATE=2) across processes: the 2MM E products
+    run their resident rows beside the copy-engine all-gather of D and the arrived rows
+    after it; everything else as in the plain two-GPU run."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, {}, gate="2")
 
 
 def test_spmd_four_gpus():
