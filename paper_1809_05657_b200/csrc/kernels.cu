@@ -757,7 +757,11 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     bx.gx[k] = (int)((c1 - bx.cbase[k] + per_block - 1) / per_block);
   }
   int64_t pb = (pull.total_units + 7) / 8;  // 8 warps per block
-  const int npull = (int)std::max<int64_t>(1, std::min<int64_t>(pb, 64));
+  // pull blocks at most (HDA_HALO_NPULL): they spin on the writers' PROD words until the
+  // neighbours finish, holding slots the interior could use; N=8-sized shares (5792^2 on
+  // 4 GPUs): 16 -> 997-1001 GPoints/s, 64 -> 969-986, 4 -> 662-670 (profiles/r02/halo_npull/)
+  static const int npull_cap = env_or("HDA_HALO_NPULL", 16);
+  const int npull = (int)std::max<int64_t>(1, std::min<int64_t>(pb, npull_cap));
   // Interior boxes: when the GPU's share is under ~5 waves of 16-row tiles, ONE wave
   // of row-range blocks sized to the slots the pull blocks leave free (blocks that
   // miss the first wave would double the step); the boundary strips keep 16-row tiles
