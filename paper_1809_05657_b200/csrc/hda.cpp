@@ -888,6 +888,13 @@ static int issue_gated_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k) 
   return HDA_OK;
 }
 
+// HDA_PULL_WAIT_KERNEL (default 1): a comm-stream SM pull waits for its writers in a
+// one-CTA launch, then copies with no waits
+static bool pull_wait_kernel_on() {
+  static const int v = env_int("HDA_PULL_WAIT_KERNEL", 1);
+  return v != 0;
+}
+
 // one device's pull (reader q = job.dst): thread-safe against the other devices' issue
 static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigned long long k, bool overlap_kernel,
                       bool halo_kernel, const double* scalars) {
@@ -940,7 +947,10 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
   int rc;
   cudaEvent_t a = nullptr;
   const size_t nb = job.batches.size();
-  if (job.ce.empty() && (rc = timed_begin(ctx, st, &a))) return rc;
+  // the exchange timer brackets the transfer, not the wait for the writers (below: the
+  // copy-engine path and the comm-stream wait launch start it after their waits)
+  const bool wait_first = nb > 0 && comm && pull_wait_kernel_on() && pre.nwait > 0;
+  if (job.ce.empty() && !wait_first && (rc = timed_begin(ctx, st, &a))) return rc;
   if (!job.ce.empty()) {  // copy-engine part: RAW wait kernel, then the copies
     KSync w = ks_empty(ctx);
     std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
@@ -965,9 +975,8 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
   // into the pull kernel, every one of its CTAs would spin on the writers' PROD words for
   // as long as the neighbours take to finish their previous step (~30 us at N=4), holding
   // SM slots the interior launch running beside it needs (HDA_PULL_WAIT_KERNEL=0: fold)
-  static const int pull_wait_kernel = env_int("HDA_PULL_WAIT_KERNEL", 1);
   bool waited_outside = false;
-  if (nb > 0 && comm && pull_wait_kernel && pre.nwait > 0) {
+  if (wait_first && pre.nwait > 0) {
     KSync w = ks_empty(ctx);
     std::memcpy(w.wait_ptr, pre.wait_ptr, sizeof w.wait_ptr);
     std::memcpy(w.wait_val, pre.wait_val, sizeof w.wait_val);
@@ -979,6 +988,7 @@ static int issue_pull(hda_ctx_t* ctx, const Transition* t, PullJob& job, unsigne
     count_launch(ctx);
     pre.nwait = 0;
     waited_outside = true;
+    if ((rc = timed_begin(ctx, st, &a))) return rc;
   }
   for (size_t i = 0; i < nb; i++) {
     KSync ks = ks_empty(ctx);
