@@ -64,6 +64,7 @@ struct Gpu {
   cudaStream_t stream = nullptr;  // compute (and everything else)
   cudaStream_t comm = nullptr;    // overlapped halo pulls
   cudaEvent_t ev_fork = nullptr, ev_pull = nullptr;
+  cudaEvent_t ev_src[kMaxGate] = {};  // gated pull: source i's block has landed
 };
 
 struct Dev {
@@ -833,8 +834,9 @@ static const MemOps& memops() {
 // HDA_GEMM_GATE: how a GEMM whose B rows arrive from other GPUs (copy-engine blocks,
 // arrival flags written by the comm stream) overlaps that all-gather.
 //   2 (default) split: with an fp32 C and whole k-blocks per source, one launch over the
-//     resident rows beside the copies, a second (C += ...) after them; otherwise joined.
-//     2MM ROW 16384^2: N=2 5.25-5.29 vs 5.51 ms per step joined, N=4 2.80 vs 3.09.
+//     resident rows beside the copies, then one (C += ...) per source as its rows land;
+//     otherwise joined.  2MM ROW 16384^2: N=2 5.09-5.12 vs 5.51 ms per step joined, N=4
+//     2.67 (2.80 with one launch for all arrived rows) vs 3.09.
 //   1 gated inside the kernel: producers wait per k-block for the sources' flags (with
 //     fp32 C, K in per-segment passes).  Slower than joining (N=2: 5.62-5.70 vs 5.40):
 //     the copies take 0.43 ms either way, the gated product 0.68 ms longer.
@@ -875,6 +877,7 @@ static int issue_gated_pull(hda_ctx_t* ctx, PullJob& job, unsigned long long k) 
     // default flags: a system-wide fence precedes each write
     CU(mo.write(cs, (CUdeviceptr)(ctx->dev[q].sync + SW_GATE + p), k, CU_STREAM_WRITE_VALUE_DEFAULT));
     CU(mo.write(cs, (CUdeviceptr)(ctx->dev[p].sync + SW_ACK + q), k, CU_STREAM_WRITE_VALUE_DEFAULT));
+    CK(cudaEventRecord(g.ev_src[i], g.comm));  // the split product's launch for these rows waits here
     kg.lo[i] = job.gate_rows[i].first;
     kg.hi[i] = job.gate_rows[i].second;
     kg.flag[i] = ctx->dev[q].sync + SW_GATE + p;
@@ -1271,8 +1274,8 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
       const TArray& B = ctx->tr->array(ci.param_array[2]);
       const int64_t K = A.shape[1];
       // HDA_GEMM_GATE=2, split form: with an fp32 C and whole k-blocks per source, the
-      // resident rows' product runs as one launch beside the copies and the arrived rows'
-      // product as a second launch after them (C += ...), no in-kernel gating
+      // resident rows' product runs as one launch beside the copies and each source's
+      // rows as a launch after its copy (C += ...), no in-kernel gating
       constexpr int64_t BK = 64;  // the CTA-pair GEMM's k-block
       if (gate && gate->n > 0 && gate_mode() == 2 && a0.dtype == HDA_F32) {
         const int64_t kb = (K + BK - 1) / BK;
@@ -1288,20 +1291,26 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
         while (b < kb && !remote[b]) b++;
         bool contiguous = a < b;
         for (int64_t x = b; x < kb; x++) contiguous &= remote[x] != 0;
-        KGate g1, g2;
+        KGate g1;
         std::memset(&g1, 0, sizeof g1);
-        std::memset(&g2, 0, sizeof g2);
         g1.nseg = 1, g1.skb0[0] = (int32_t)a, g1.skb1[0] = (int32_t)b;
-        if (a > 0) g2.skb0[g2.nseg] = 0, g2.skb1[g2.nseg++] = (int32_t)a;
-        if (b < kb) g2.skb0[g2.nseg] = (int32_t)b, g2.skb1[g2.nseg++] = (int32_t)kb;
-        if (aligned && contiguous && g2.nseg > 0) {
+        if (aligned && contiguous && b - a < kb) {
           cudaError_t e = launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
                                       (float)scalars[0], (float)scalars[1], ks_part(ctx, ks, true, false), s, &g1);
           if (e == cudaSuccess) {
-            count_launch(ctx);
-            CK(cudaStreamWaitEvent(s, ctx->gpus[ctx->dev[q].gpu].ev_pull, 0));
-            CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
-                           (float)scalars[0], 1.0f, ks_part(ctx, ks, false, true), s, &g2));
+            // then one launch per source, in arrival order, as its rows land (C += ...)
+            const Gpu& gg = ctx->gpus[ctx->dev[q].gpu];
+            for (int i = 0; i < gate->n; i++) {
+              count_launch(ctx);
+              KGate gi;
+              std::memset(&gi, 0, sizeof gi);
+              gi.nseg = 1;
+              gi.skb0[0] = (int32_t)(gate->lo[i] / BK);
+              gi.skb1[0] = (int32_t)std::min<int64_t>(kb, (gate->hi[i] + BK - 1) / BK);
+              CK(cudaStreamWaitEvent(s, gg.ev_src[i], 0));
+              CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
+                             (float)scalars[0], 1.0f, ks_part(ctx, ks, false, i + 1 == gate->n), s, &gi));
+            }
             __atomic_fetch_add(&ctx->stats.gated_products, (int64_t)1, __ATOMIC_RELAXED);
             break;
           }
@@ -1712,6 +1721,7 @@ static int setup_gpu_common(hda_ctx_t* ctx) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&g.comm, cudaStreamNonBlocking, hi));
     CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+    for (cudaEvent_t& e : g.ev_src) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g.ev_pull, cudaEventDisableTiming));
   }
   CK(cudaHostAlloc((void**)&ctx->err_host, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1837,6 +1847,8 @@ int hda_finalize(hda_ctx_t* ctx) {
       cudaStreamDestroy(gp.comm);
       cudaEventDestroy(gp.ev_fork);
       cudaEventDestroy(gp.ev_pull);
+      for (cudaEvent_t e : gp.ev_src)
+        if (e) cudaEventDestroy(e);
     }
     if (ctx->err_host) cudaFreeHost(ctx->err_host);
   }
