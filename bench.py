@@ -438,8 +438,8 @@ class TwoMM:
         self.kind = "2mm"
         self.workload = (f"SURVEY 8(f)-1 2MM chain (P:L425): D=AxB, E=CxD, {n}^2 bf16 in, D bf16, E fp32, "
                          f"{part.upper()} partition")
-        self.kname = ("gemm2_kernel (tcgen05 cta_group::2), two launches per step" if _env_int("HDA_GEMM_2SM", 1)
-                      else "gemm_kernel (tcgen05), two launches per step")
+        self.kname = ("gemm2_kernel (tcgen05 cta_group::2), two products per step" if _env_int("HDA_GEMM_2SM", 1)
+                      else "gemm_kernel (tcgen05), two products per step")
         self.dtype_name = "bf16"
         self.metric_unit = "TFLOP/s"
         self.flops_per_step = 4.0 * n ** 3
