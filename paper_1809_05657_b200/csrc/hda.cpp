@@ -1172,6 +1172,56 @@ static KSync ks_part(hda_ctx_t* ctx, const KSync& ks, bool first, bool last) {
   return k2;
 }
 
+// HDA_GEMM_GATE=2, the split product (all-gather of B overlapped with the GEMM): with an
+// fp32 C and whole k-blocks per source, the resident rows' product runs as one launch
+// beside the copy-engine blocks, then one launch (C += alpha * A_i B_i) per source, in
+// arrival order, each after the comm-stream event behind that source's block.  No
+// in-kernel gating.  *done = false (nothing launched) when the resident rows are not one
+// contiguous run of whole k-blocks or the CTA-pair kernel does not apply; the caller
+// then joins the copies.
+static int split_product(hda_ctx_t* ctx, int q, const void* A, const void* B, void* C, int64_t M, int64_t N,
+                         int64_t K, const Box& fb, float alpha, float beta, const KSync& ks, cudaStream_t s,
+                         const KGate& gate, bool* done) {
+  constexpr int64_t BK = 64;  // the CTA-pair GEMM's k-block
+  *done = false;
+  const int64_t kb = (K + BK - 1) / BK;
+  std::vector<char> remote(kb, 0);
+  bool aligned = true;
+  for (int i = 0; i < gate.n; i++) {
+    if (gate.lo[i] % BK || (gate.hi[i] % BK && gate.hi[i] != K)) aligned = false;
+    for (int64_t b = gate.lo[i] / BK; b * BK < gate.hi[i] && b < kb; b++) remote[b] = 1;
+  }
+  int64_t a = 0;  // resident k-blocks [a, b)
+  while (a < kb && remote[a]) a++;
+  int64_t b = a;
+  while (b < kb && !remote[b]) b++;
+  bool contiguous = a < b;
+  for (int64_t x = b; x < kb; x++) contiguous &= remote[x] != 0;
+  if (!aligned || !contiguous || b - a >= kb) return HDA_OK;
+  KGate g1;
+  std::memset(&g1, 0, sizeof g1);
+  g1.nseg = 1, g1.skb0[0] = (int32_t)a, g1.skb1[0] = (int32_t)b;
+  const cudaError_t e = launch_gemm(HDA_F32, A, B, C, M, N, K, fb.lb, fb.ub, alpha, beta,
+                                    ks_part(ctx, ks, true, false), s, &g1);
+  if (e == cudaErrorNotSupported) return HDA_OK;
+  CK(e);
+  const Gpu& gg = ctx->gpus[ctx->dev[q].gpu];
+  for (int i = 0; i < gate.n; i++) {
+    count_launch(ctx);  // the previous launch (the caller counts the last one)
+    KGate gi;
+    std::memset(&gi, 0, sizeof gi);
+    gi.nseg = 1;
+    gi.skb0[0] = (int32_t)(gate.lo[i] / BK);
+    gi.skb1[0] = (int32_t)std::min<int64_t>(kb, (gate.hi[i] + BK - 1) / BK);
+    CK(cudaStreamWaitEvent(s, gg.ev_src[i], 0));
+    CK(launch_gemm(HDA_F32, A, B, C, M, N, K, fb.lb, fb.ub, alpha, 1.0f, ks_part(ctx, ks, false, i + 1 == gate.n),
+                   s, &gi));
+  }
+  __atomic_fetch_add(&ctx->stats.gated_products, (int64_t)1, __ATOMIC_RELAXED);
+  *done = true;
+  return HDA_OK;
+}
+
 static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* scalars, const KSync& ks,
                       const std::vector<Box>* boxes, cudaStream_t stream, const KGate* gate) {
   const CallInfo& ci = *t->info;
@@ -1273,49 +1323,12 @@ static int run_kernel(hda_ctx_t* ctx, const Transition* t, int q, const double* 
       const TArray& A = ctx->tr->array(ci.param_array[1]);
       const TArray& B = ctx->tr->array(ci.param_array[2]);
       const int64_t K = A.shape[1];
-      // HDA_GEMM_GATE=2, split form: with an fp32 C and whole k-blocks per source, the
-      // resident rows' product runs as one launch beside the copies and each source's
-      // rows as a launch after its copy (C += ...), no in-kernel gating
-      constexpr int64_t BK = 64;  // the CTA-pair GEMM's k-block
       if (gate && gate->n > 0 && gate_mode() == 2 && a0.dtype == HDA_F32) {
-        const int64_t kb = (K + BK - 1) / BK;
-        std::vector<char> remote(kb, 0);
-        bool aligned = true;
-        for (int i = 0; i < gate->n; i++) {
-          if (gate->lo[i] % BK || (gate->hi[i] % BK && gate->hi[i] != K)) aligned = false;
-          for (int64_t b = gate->lo[i] / BK; b * BK < gate->hi[i] && b < kb; b++) remote[b] = 1;
-        }
-        int64_t a = 0;
-        while (a < kb && remote[a]) a++;
-        int64_t b = a;
-        while (b < kb && !remote[b]) b++;
-        bool contiguous = a < b;
-        for (int64_t x = b; x < kb; x++) contiguous &= remote[x] != 0;
-        KGate g1;
-        std::memset(&g1, 0, sizeof g1);
-        g1.nseg = 1, g1.skb0[0] = (int32_t)a, g1.skb1[0] = (int32_t)b;
-        if (aligned && contiguous && b - a < kb) {
-          cudaError_t e = launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
-                                      (float)scalars[0], (float)scalars[1], ks_part(ctx, ks, true, false), s, &g1);
-          if (e == cudaSuccess) {
-            // then one launch per source, in arrival order, as its rows land (C += ...)
-            const Gpu& gg = ctx->gpus[ctx->dev[q].gpu];
-            for (int i = 0; i < gate->n; i++) {
-              count_launch(ctx);
-              KGate gi;
-              std::memset(&gi, 0, sizeof gi);
-              gi.nseg = 1;
-              gi.skb0[0] = (int32_t)(gate->lo[i] / BK);
-              gi.skb1[0] = (int32_t)std::min<int64_t>(kb, (gate->hi[i] + BK - 1) / BK);
-              CK(cudaStreamWaitEvent(s, gg.ev_src[i], 0));
-              CK(launch_gemm(a0.dtype, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb.lb, fb.ub,
-                             (float)scalars[0], 1.0f, ks_part(ctx, ks, false, i + 1 == gate->n), s, &gi));
-            }
-            __atomic_fetch_add(&ctx->stats.gated_products, (int64_t)1, __ATOMIC_RELAXED);
-            break;
-          }
-          if (e != cudaErrorNotSupported) CK(e);
-        }
+        bool done = false;
+        int rc = split_product(ctx, q, P_(1), P_(2), P_(0), A.shape[0], B.shape[1], K, fb, (float)scalars[0],
+                               (float)scalars[1], ks, s, *gate, &done);
+        if (rc) return rc;
+        if (done) break;
       }
       if (gate && gate_mode() == 2) {  // not splittable: join the copies first
         CK(cudaStreamWaitEvent(s, ctx->gpus[ctx->dev[q].gpu].ev_pull, 0));
