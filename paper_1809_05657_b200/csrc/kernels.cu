@@ -829,7 +829,11 @@ static cudaError_t launch_halo_t(const T* in, T* out, const int64_t* shape, cons
     bx.tstart[k + 1] = bx.tstart[k] + (int64_t)bx.gx[k] * bx.gy[k];
   }
   bx.ndep_first = 0;
-  bx.pf = st_prefetch(KIND);
+  // no L2 prefetch in the fused halo launch (HDA_HALO_PF): forced onto 268 MB shares
+  // (8192^2, N=4) it costs 998 vs 1172 GPoints/s; on the 134 MB shares the fused launch is
+  // chosen for, 990 without vs 997-1001 with (separate boxes; within 1%, profiles/r02/halo_pf/)
+  static const int halo_pf = env_or("HDA_HALO_PF", 0);
+  bx.pf = halo_pf;
   if (dep_first && ni < bx.n) {  // rotate the boundary boxes to the front
     Boxes2 o = bx;
     int j = 0;
