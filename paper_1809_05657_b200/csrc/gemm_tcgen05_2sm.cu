@@ -199,7 +199,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int64_t tiles_m = (m1 - m0 + 2 * BM - 1) / (2 * BM), tiles_n = (n1 - nbase + BN - 1) / BN;
   const int64_t n_tiles = tiles_m * tiles_n;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int kblocks = (int)((K + BK - 1) / BK);
   // K segments (KGate): one pass over the tiles per segment when the output is fp32 and
   // the launch is gated (each pass accumulates into C), else one pass over all of them
   const bool multi = gate.multi != 0;
