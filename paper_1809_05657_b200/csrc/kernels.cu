@@ -331,7 +331,13 @@ static int tail_waves() {
 
 constexpr int ST_THREADS = 256;  // threads per block along the row
 constexpr int ST_GROUP = 4;      // rows loaded together (loads in flight per thread)
-constexpr int ST_ROWS = 16;      // rows per block
+#ifndef ST_ROWS_DEF
+#define ST_ROWS_DEF 16
+#endif
+constexpr int ST_ROWS = ST_ROWS_DEF;  // rows per block (16-row tiles)
+#ifndef ST9_ROWS
+#define ST9_ROWS 32  // the 9-point kernel's tile height (plain launches)
+#endif
 constexpr int ST_MINB = 4;       // resident blocks per SM (register cap)
 #ifndef ST9_MINB
 // the 9-point kernel's register cap (blocks per SM): 5 spilled (48 registers); with the
@@ -672,7 +678,16 @@ static cudaError_t launch_stencil2d_t(const T* in, T* out, const int64_t* shape,
     bx.tstart[0] = 0;
     for (int k = 0; k < bx.n; k++) {
       const int64_t rows = bx.r1[k] - bx.r0[k];
-      int64_t gyk = (rows + ST_ROWS - 1) / ST_ROWS;
+      // tile height: 16 rows, or ST9_ROWS (32) for a wide 9-point box that still spans
+      // >= 10 waves of them.  16384^2 9-point (profiles/r02/stencil9_rows/): N=1 (28
+      // waves) 385.5 vs 376.6 GPoints/s, N=2 (14) 728 vs 696-702; N=4 (7 waves) 1225 vs
+      // 1259 with 32.  64 rows: 371.3 at N=1.  The 5-point loses at 32 (367.7 vs 399.8).
+      // Narrow boxes (a BLOCK halo's column strips, one live thread per block) keep 16.
+      int64_t trows = ST_ROWS;
+      if (KIND == 1 && bx.c1[k] - bx.c0[k] > 64 &&
+          (int64_t)bx.gx[k] * ((rows + ST9_ROWS - 1) / ST9_ROWS) >= 10 * wave)
+        trows = ST9_ROWS;
+      int64_t gyk = (rows + trows - 1) / trows;
       if (one_wave && bx.c1[k] - bx.c0[k] > 64) {
         gyk = std::max<int64_t>(1, wave / std::max<int64_t>(strips, 1));
         gyk = std::min<int64_t>(gyk, (rows + ST_GROUP - 1) / ST_GROUP);
